@@ -1,0 +1,288 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 IT-MPPI hot path (one IT-MPPI iteration = one step).
+
+Workload (BASELINE.json configs[1], "c1"): K = 16384 samples, T = 100, 6-32-32-4
+tanh MLP vehicle, 2000 x 2000 elliptical-track costmap, receding horizon with
+the device plant; all inputs synthetic from a seed (see
+paper_1707_02342_b200/workload.py).  Samples shard over the ranks of a
+torchrun launch (one NCCL all-gather of per-chunk softmin partials per
+iteration); ``value`` is whole-job sample-timesteps/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPPI iteration latency (ms) and rollout sample-timesteps/sec at 1/2/4/8 B200"
+UNIT = "sample-timesteps/s"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--samples", type=int, default=None, help="override K (c4 sweep)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_cpu(w, steps, warmup, sample_k):
+    """The reference CPU path (oracle restatement: double, splitmix noise, std::thread
+    chunks per call, serial sampling/weights/update) on a bounded sample of the workload."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle  # test infrastructure; the CPU arm only
+    from paper_1707_02342_b200.api import SamplingParams
+    p = SamplingParams(**{**w.params.__dict__, "samples": sample_k})
+    o = oracle.OracleController(p, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp64", noise="ref_splitmix")
+    o.set_mlp(w.mlp)
+    o.set_costmap(w.costmap)
+    threads = cpu_threads()
+    x = w.x0[0].copy()
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        u = o.mpc_step(x, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+        x = o.vehicle_step(x, u)
+    med = statistics.median(times)
+    return {"value": sample_k * w.params.horizon_steps / med, "unit": UNIT, "cores": threads, "kind": "port",
+            "ms_per_step": med * 1e3, "total_s": sum(times),
+            "sample": f"{len(times)} mpc_step calls on {sample_k} of the {w.params.samples} samples, "
+                      f"T={w.params.horizon_steps}, fp64, reference splitmix noise, {threads} std::threads"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1707_02342_b200 import workload
+    w = workload.make(args.config, samples=args.samples)
+    sample_k = min(w.params.samples, 2048)
+    steps = max(1, min(args.steps, 60))
+    warm = max(1, min(args.warmup, 3))
+    cb = reference_cpu(w, steps, warm, sample_k)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": cb["ms_per_step"] * (w.params.samples / sample_k),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config}: K={w.params.samples}, T={w.params.horizon_steps}, H={w.hidden}",
+                       "parallelism": f"{cb['cores']} CPU threads"},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_rollout_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch"), d.get("source")
+    except Exception:
+        return None, None
+
+
+def run_ours(args):
+    import torch
+    from paper_1707_02342_b200 import workload
+    from paper_1707_02342_b200.api import Controller, fp32_peak_tflops
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+
+    w = workload.make(args.config, samples=args.samples)
+    ctrl = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox",
+                      device=local, n_controllers=1)
+    ctrl.set_mlp(w.mlp)
+    ctrl.set_costmap(w.costmap)
+    if world > 1:
+        obj = [Controller.nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        ctrl.set_comm(rank, world, obj[0])
+    K, T = w.params.samples, w.params.horizon_steps
+    x0 = w.x0[0]
+    stream = torch.cuda.ExternalStream(ctrl.stream)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (graphs captured, clocks up)
+    ctrl.closed_loop_timed(x0, max(3, args.warmup), L2_FLUSH_BYTES)
+    ctrl.profile_read(reset=True)
+    barrier()
+    n_launch0 = ctrl.launch_count
+    with ClockSampler(local) as clocks:
+        ms = ctrl.closed_loop_timed(x0, args.steps, L2_FLUSH_BYTES)
+    barrier()
+    launches = ctrl.launch_count - n_launch0
+    k1_ms, k1_n = ctrl.profile_read(reset=True)
+    t = torch.tensor([ms, k1_ms / max(k1_n, 1)], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    ms_max, k1_avg_ms = float(t[0]), float(t[1])
+    ms_per_step = ms_max / args.steps
+    value = K * T * args.steps / (ms_max * 1e-3)  # all ranks together process K samples per iteration
+
+    # end to end through the public API: host x0 -> H2D, step, D2H u0, every step
+    e2e = None
+    if not args.no_e2e:
+        x = x0.copy()
+        for _ in range(3):
+            ctrl.mpc_step(x)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            u = ctrl.mpc_step(x)
+            # host plant (outside the controller): kinematic pose update, the
+            # executed throttle nudges v_x
+            x[0] += (np.cos(x[2]) * x[4] - np.sin(x[2]) * x[5]) * w.params.dt
+            x[1] += (np.sin(x[2]) * x[4] + np.cos(x[2]) * x[5]) * w.params.dt
+            x[2] += x[6] * w.params.dt
+            x[4] += 0.5 * u[1] * w.params.dt
+        ev1.record(stream)
+        ev1.synchronize()
+        e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+        if pg:
+            pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
+        e_ms = float(e_ms[0])
+        e2e = {"value": K * T * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
+               "h2d_bytes_per_step": 8 * 4, "d2h_bytes_per_step": 96,
+               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H"}
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    flop_unit = workload.flops_per_sample_step(w.hidden)
+    k_local = K // world if world > 1 else K
+    k1_flops = k_local * T * flop_unit
+    peak, clk = fp32_peak_tflops(local)
+    achieved = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else None
+    traffic, traffic_src = load_traffic()
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cb = reference_cpu(w, steps=3, warmup=1, sample_k=min(K, 2048))
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Xavier MLP, 2000x2000 ellipse map, Philox noise)",
+        "config": {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, H={w.hidden}, MLP vehicle, "
+                               f"receding horizon with device plant",
+                   "samples": K, "horizon": T, "hidden": w.hidden, "parallelism": f"samples sharded over {world} GPU(s)",
+                   "l2": "flushed between timed iterations (256 MiB memset, excluded from timing)",
+                   "kernel": ctrl.kernel_variant},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+                     "kernel": "rollout_kernel (K1)", "k1_ms_per_launch": k1_avg_ms,
+                     "k1_share_of_step": k1_avg_ms / ms_per_step if ms_per_step else None,
+                     "flop_per_launch": k1_flops, "flop_per_sample_step": flop_unit,
+                     "peak_source": "measured FFMA/FFMA2 probe on this GPU (mppi_gpu_fp32_peak_probe); "
+                                    "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
+                     "traffic_source": traffic_src},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+        "iteration_latency_ms": ms_per_step,
+    }
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

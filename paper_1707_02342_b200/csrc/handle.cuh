@@ -1,0 +1,946 @@
+// handle.cuh — the controller handle for one arithmetic type R: device
+// buffers, launch plumbing, captured CUDA graphs and the NCCL sample-shard
+// exchange.  Instantiated once per precision (handle_f32.cu, handle_f64.cu).
+//
+// The host side of the drop-in boundary.  It owns all device memory of one
+// control loop (or fleet), one CUDA stream, the captured CUDA graphs of the
+// iteration, and (multi-GPU) the NCCL communicator of its sample shard.  No
+// CPU fallback exists: every compute entry point launches device kernels and
+// fails with MPPI_ERR_CUDA when no device is usable.
+#pragma once
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "epilogue.cuh"
+#include "errors.hpp"
+#include "handle_iface.hpp"
+#include "host_util.hpp"
+#include "nccl_api.hpp"
+
+namespace mppi_host {
+
+using namespace mppi_dev;
+
+// -------------------------------------------------------- device buffers ----
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+};
+template <class T>
+struct HostPinned {
+  T* p = nullptr;
+  size_t n = 0;
+  ~HostPinned() {
+    if (p) cudaFreeHost(p);
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    CUDA_TRY(cudaMallocHost(&p, count * sizeof(T)));
+    n = count;
+  }
+};
+
+constexpr int kBlock = 128;      // samples per chunk / K1 CTA
+constexpr int kEpiBlock = 512;   // K2 CTA
+
+template <class R>
+struct Handle final : HandleBase {
+  // ---- HandleBase adaptors
+  int device_index() const override { return device; }
+  int controllers() const override { return C; }
+  const mppi_gpu_config& config() const override { return cfg; }
+  void set_map_f64(int c, const double* v, int w, int h, double x0, double y0, double res) override {
+    set_map(c, v, w, h, x0, y0, res);
+  }
+  void set_map_f32(int c, const float* v, int w, int h, double x0, double y0, double res) override {
+    set_map(c, v, w, h, x0, y0, res);
+  }
+  void* stream_ptr() const override { return reinterpret_cast<void*>(stream); }
+  uint64_t launch_count() const override { return launches; }
+  void set_profile(bool on) override { profile = on; }
+  void read_profile(double* ms, uint64_t* n, bool reset) override {
+    if (ms) *ms = prof_ms;
+    if (n) *n = prof_launches;
+    if (reset) {
+      prof_ms = 0;
+      prof_launches = 0;
+    }
+  }
+  std::string variant_name() const override {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
+                  std::is_same<R, double>::value ? "f64" : "f32", H,
+                  cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic" : "vehicle_mlp", cfg.noise_mode, kBlock);
+    return buf;
+  }
+
+  mppi_gpu_config cfg{};
+  int K = 0, T = 0, C = 1, H = 32, device = 0;
+  int n_chunks = 0, chunks_per_rank = 0, chunk_lo = 0, chunk_hi = 0;
+  int rank = 0, world = 1;
+  int zero_start = 0;
+  int partial_stride = 0;
+  long long partials_ctrl_stride = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<double> sg;
+  uint64_t launches = 0;
+
+  // weights (host copies; by-value kernel parameters) + device copy for the
+  // by-pointer variant
+  std::unique_ptr<MlpParams<R, 32>> w32;
+  std::unique_ptr<MlpParams<R, 64>> w64;
+  DevBuf<MlpParams<R, 64>> d_w64;
+  bool has_mlp = false, has_map = false, has_noise = false;
+
+  // device state
+  DevBuf<R> d_plan, d_x0, d_costs, d_partials, d_inj, d_decay, d_agg, d_w, d_rho_eta;
+  DevBuf<R> d_states, d_utrace, d_xtrace;
+  DevBuf<double> d_eps_ref;
+  DevBuf<uint64_t> d_iters, d_seeds, d_trace_base;
+  DevBuf<int> d_abort, d_bad;
+  DevBuf<StepStatus> d_status;
+  DevBuf<const R*> d_map_ptrs;
+  DevBuf<R> d_map_shared;
+  std::vector<std::unique_ptr<DevBuf<R>>> d_map_fleet;
+  DevBuf<unsigned char> d_flush;
+  int map_w = 0, map_h = 0;
+  double map_x0 = 0, map_y0 = 0, map_res = 1;
+  HostPinned<R> h_x0;
+  HostPinned<StepStatus> h_status;
+  std::vector<uint64_t> h_iters;
+
+  // last parity batch (for update_plan / rollout_states)
+  bool batch_valid = false, batch_injected = false;
+  uint64_t batch_iteration = 0;
+
+  // profiling
+  bool profile = false;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_it0 = nullptr, ev_it1 = nullptr;
+  double prof_ms = 0;
+  uint64_t prof_launches = 0;
+
+  // graphs: 0 = step (compute+slide), 1 = compute only, 2 = closed-loop iteration
+  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  bool graph_trace[3] = {false, false, false};
+
+  explicit Handle(const mppi_gpu_config& c) : cfg(c) {
+    validate_config(c);
+    K = c.samples;
+    T = c.horizon_steps;
+    C = c.n_controllers;
+    H = c.mlp_hidden;
+    device = c.device;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw Error(MPPI_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev) throw_invalid("config.device out of range");
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&ev_a));
+    CUDA_TRY(cudaEventCreate(&ev_b));
+    CUDA_TRY(cudaEventCreate(&ev_it0));
+    CUDA_TRY(cudaEventCreate(&ev_it1));
+    n_chunks = (K + kBlock - 1) / kBlock;
+    chunks_per_rank = n_chunks;
+    chunk_lo = 0;
+    chunk_hi = n_chunks;
+    zero_start = K - static_cast<int>(std::lround(c.explore_fraction * K));
+    partial_stride = kPartialHeader + 2 * T;
+    partials_ctrl_stride = static_cast<long long>(n_chunks) * partial_stride;
+    if (c.sg_window != 0) sg = mppi_host::sg_coefficients(c.sg_window, c.sg_degree);
+
+    d_plan.alloc(static_cast<size_t>(C) * 2 * T);
+    CUDA_TRY(cudaMemset(d_plan.p, 0, d_plan.n * sizeof(R)));
+    d_x0.alloc(static_cast<size_t>(C) * 8);
+    CUDA_TRY(cudaMemset(d_x0.p, 0, d_x0.n * sizeof(R)));
+    d_costs.alloc(static_cast<size_t>(C) * K);
+    d_partials.alloc(static_cast<size_t>(C) * partials_ctrl_stride);
+    d_agg.alloc(static_cast<size_t>(2) * T);
+    d_iters.alloc(C);
+    CUDA_TRY(cudaMemset(d_iters.p, 0, C * sizeof(uint64_t)));
+    h_iters.assign(C, 0);
+    d_trace_base.alloc(C);
+    d_seeds.alloc(C);
+    std::vector<uint64_t> seeds(C);
+    for (int i = 0; i < C; ++i) seeds[i] = c.seed + static_cast<uint64_t>(i);
+    CUDA_TRY(cudaMemcpy(d_seeds.p, seeds.data(), C * sizeof(uint64_t), cudaMemcpyHostToDevice));
+    d_abort.alloc(C);
+    CUDA_TRY(cudaMemset(d_abort.p, 0, C * sizeof(int)));
+    d_bad.alloc(1);
+    d_rho_eta.alloc(2);
+    d_status.alloc(C);
+    CUDA_TRY(cudaMemset(d_status.p, 0, C * sizeof(StepStatus)));
+    h_status.alloc(C);
+    h_x0.alloc(static_cast<size_t>(C) * 8);
+    std::memset(h_x0.p, 0, sizeof(R) * C * 8);
+    // decay^t table (std::pow, costs.cpp:35)
+    std::vector<R> decay(T + 1);
+    for (int t = 0; t <= T; ++t) decay[t] = static_cast<R>(std::pow(c.cost.decay, t));
+    d_decay.alloc(T + 1);
+    CUDA_TRY(cudaMemcpy(d_decay.p, decay.data(), (T + 1) * sizeof(R), cudaMemcpyHostToDevice));
+    d_map_ptrs.alloc(C);
+    CUDA_TRY(cudaMemset(d_map_ptrs.p, 0, C * sizeof(const R*)));
+    if (c.system == MPPI_SYSTEM_QUADRATIC) has_mlp = true, has_map = true;
+    w32 = std::make_unique<MlpParams<R, 32>>();
+    w64 = std::make_unique<MlpParams<R, 64>>();
+    std::memset(w32.get(), 0, sizeof(MlpParams<R, 32>));
+    std::memset(w64.get(), 0, sizeof(MlpParams<R, 64>));
+  }
+
+  ~Handle() override {
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
+    if (comm) nccl().CommDestroy(comm);
+    if (ev_a) cudaEventDestroy(ev_a);
+    if (ev_b) cudaEventDestroy(ev_b);
+    if (ev_it0) cudaEventDestroy(ev_it0);
+    if (ev_it1) cudaEventDestroy(ev_it1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  static void validate_config(const mppi_gpu_config& c) {
+    // SamplingParams::validate (types.hpp:105-122)
+    if (c.samples < 1) throw_invalid("SamplingParams: samples must be >= 1");
+    if (c.horizon_steps < 1) throw_invalid("SamplingParams: horizon_steps must be >= 1");
+    if (!(c.dt > 0.0)) throw_invalid("SamplingParams: dt must be > 0");
+    for (int i = 0; i < 2; ++i)
+      if (!(c.sigma_diag[i] > 0.0) || !std::isfinite(c.sigma_diag[i]))
+        throw_invalid("SamplingParams: sigma_diag entries must be finite and > 0");
+    if (!(c.lambda > 0.0)) throw_invalid("SamplingParams: lambda must be > 0");
+    if (!(c.gamma >= 0.0)) throw_invalid("SamplingParams: gamma must be >= 0");
+    if (!(c.explore_fraction >= 0.0 && c.explore_fraction < 1.0))
+      throw_invalid("SamplingParams: explore_fraction must be in [0, 1)");
+    // ControlBounds::validate (dynamics.hpp:19-28)
+    for (int i = 0; i < 2; ++i)
+      if (!(c.bounds_lower[i] < c.bounds_upper[i])) throw_invalid("ControlBounds: lower must be < upper");
+    if (c.sg_window != 0) {
+      if (c.sg_window < 3 || c.sg_window % 2 == 0) throw_invalid("sg_coefficients: window must be odd and >= 3");
+      if (c.sg_degree < 0 || c.sg_degree >= c.sg_window) throw_invalid("sg_coefficients: need 0 <= degree < window");
+      if (c.sg_window > kMaxSgWindow) throw Error(MPPI_ERR_UNSUPPORTED, "sg window > 63");
+    }
+    if (c.weight_rule != MPPI_WEIGHT_IT)
+      throw Error(MPPI_ERR_UNSUPPORTED, "only the information-theoretic weight rule runs on the device");
+    if (c.noise_mode < 0 || c.noise_mode > 2) throw_invalid("noise_mode");
+    if (c.precision != MPPI_FP32 && c.precision != MPPI_FP64) throw_invalid("precision");
+    if (c.system != MPPI_SYSTEM_VEHICLE_MLP && c.system != MPPI_SYSTEM_QUADRATIC) throw_invalid("system");
+    if (c.mlp_hidden != 32 && c.mlp_hidden != 64) throw_invalid("mlp_hidden must be 32 or 64");
+    if (c.n_controllers < 1) throw_invalid("n_controllers must be >= 1");
+    if (c.noise_mode == MPPI_NOISE_INJECTED && c.n_controllers != 1)
+      throw Error(MPPI_ERR_UNSUPPORTED, "injected noise supports one controller per handle");
+    if (c.horizon_steps > 4096) throw Error(MPPI_ERR_UNSUPPORTED, "horizon_steps > 4096");
+    if (!(c.cost.decay > 0.0 && c.cost.decay <= 1.0)) throw_invalid("CostParams: decay must be in (0, 1]");
+    if (!(c.cost.alpha_track >= 0.0 && c.cost.alpha_speed >= 0.0 && c.cost.alpha_stab >= 0.0))
+      throw_invalid("CostParams: weights must be >= 0");
+  }
+
+  int state_dim() const { return cfg.system == MPPI_SYSTEM_QUADRATIC ? 2 : 7; }
+  void check_ctrl(int c) const {
+    if (c < 0 || c >= C) throw_invalid("controller index out of range");
+  }
+  void invalidate_graphs() {
+    for (auto& g : graph)
+      if (g) {
+        cudaGraphExecDestroy(g);
+        g = nullptr;
+      }
+  }
+  void require_ready() const {
+    if (!has_mlp) throw_invalid("vehicle system: MLP weights not set");
+    if (!has_map) throw_invalid("vehicle system: costmap not set");
+    if (cfg.noise_mode == MPPI_NOISE_INJECTED && !has_noise) throw_invalid("INJECTED noise: no batch set");
+  }
+
+  // ----------------------------------------------------------- set data ---
+  void set_mlp(int hidden, const double* w1, const double* b1, const double* w2, const double* b2,
+               const double* w3, const double* b3) {
+    if (cfg.system != MPPI_SYSTEM_VEHICLE_MLP) throw_invalid("set_dynamics_mlp: system has no MLP");
+    if (hidden != H) throw_invalid("set_dynamics_mlp: hidden size must match config.mlp_hidden");
+    auto fill = [&](auto& w) {
+      for (int j = 0; j < H; ++j) {
+        for (int i = 0; i < 6; ++i) w.w1t[i][j] = static_cast<R>(w1[j * 6 + i]);
+        w.b1[j] = static_cast<R>(b1[j]);
+        w.b2[j] = static_cast<R>(b2[j]);
+        for (int i = 0; i < H; ++i) w.w2t[i][j] = static_cast<R>(w2[j * H + i]);
+      }
+      for (int o = 0; o < 4; ++o) {
+        w.b3[o] = static_cast<R>(b3[o]);
+        for (int i = 0; i < H; ++i) w.w3t[i][o] = static_cast<R>(w3[o * H + i]);
+      }
+    };
+    for (int i = 0; i < H * 6; ++i)
+      if (!std::isfinite(w1[i])) throw_invalid("MLP weights must be finite");
+    if (H == 32) {
+      fill(*w32);
+    } else {
+      fill(*w64);
+      if (!kWeightsByValue<R, 64>) {
+        d_w64.alloc(1);
+        CUDA_TRY(cudaMemcpy(d_w64.p, w64.get(), sizeof(MlpParams<R, 64>), cudaMemcpyHostToDevice));
+      }
+    }
+    has_mlp = true;
+    invalidate_graphs();
+  }
+
+  template <class Src>
+  void set_map(int ctrl, const Src* values, int width, int height, double x0, double y0, double res) {
+    if (cfg.system != MPPI_SYSTEM_VEHICLE_MLP) throw_invalid("set_costmap: system has no costmap");
+    // CostMap::validate (costs.hpp:24-37)
+    if (width < 2 || height < 2) throw_invalid("CostMap: width and height must be >= 2");
+    if (!(res > 0.0)) throw_invalid("CostMap: resolution must be > 0");
+    if (has_map && (width != map_w || height != map_h || x0 != map_x0 || y0 != map_y0 || res != map_res))
+      throw_invalid("set_costmap: all maps of a handle share one geometry");
+    const size_t n = static_cast<size_t>(width) * height;
+    std::vector<R> v(n);
+    for (size_t i = 0; i < n; ++i) {
+      const double d = static_cast<double>(values[i]);
+      if (!std::isfinite(d) || std::abs(d) > 2.5) throw_invalid("CostMap: values must be finite and within +-2.5");
+      v[i] = static_cast<R>(d);
+    }
+    map_w = width;
+    map_h = height;
+    map_x0 = x0;
+    map_y0 = y0;
+    map_res = res;
+    std::vector<const R*> ptrs(C);
+    CUDA_TRY(cudaMemcpy(ptrs.data(), d_map_ptrs.p, C * sizeof(const R*), cudaMemcpyDeviceToHost));
+    if (ctrl < 0) {
+      d_map_shared.alloc(n);
+      CUDA_TRY(cudaMemcpy(d_map_shared.p, v.data(), n * sizeof(R), cudaMemcpyHostToDevice));
+      d_map_fleet.clear();
+      for (int c = 0; c < C; ++c) ptrs[c] = d_map_shared.p;
+    } else {
+      check_ctrl(ctrl);
+      if (d_map_fleet.size() != static_cast<size_t>(C)) d_map_fleet.resize(C);
+      if (!d_map_fleet[ctrl]) d_map_fleet[ctrl] = std::make_unique<DevBuf<R>>();
+      d_map_fleet[ctrl]->alloc(n);
+      CUDA_TRY(cudaMemcpy(d_map_fleet[ctrl]->p, v.data(), n * sizeof(R), cudaMemcpyHostToDevice));
+      ptrs[ctrl] = d_map_fleet[ctrl]->p;
+    }
+    CUDA_TRY(cudaMemcpy(d_map_ptrs.p, ptrs.data(), C * sizeof(const R*), cudaMemcpyHostToDevice));
+    bool all = true;
+    for (int c = 0; c < C; ++c) all = all && ptrs[c] != nullptr;
+    has_map = all;
+    invalidate_graphs();
+  }
+
+  void perturb_fleet(double sigma, uint64_t seed) {
+    if (!d_map_shared.p) throw_invalid("perturb_fleet_costmaps: set a shared costmap first");
+    if (!(sigma >= 0.0)) throw_invalid("perturb_fleet_costmaps: sigma must be >= 0");
+    const size_t n = static_cast<size_t>(map_w) * map_h;
+    d_map_fleet.clear();
+    d_map_fleet.resize(C);
+    std::vector<const R*> ptrs(C);
+    for (int c = 0; c < C; ++c) {
+      d_map_fleet[c] = std::make_unique<DevBuf<R>>();
+      d_map_fleet[c]->alloc(n);
+      perturb_map_kernel<R><<<592, 256, 0, stream>>>(d_map_shared.p, n, c, sigma, seed, d_map_fleet[c]->p);
+      ++launches;
+      CUDA_TRY(cudaGetLastError());
+      ptrs[c] = d_map_fleet[c]->p;
+    }
+    CUDA_TRY(cudaMemcpyAsync(d_map_ptrs.p, ptrs.data(), C * sizeof(const R*), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    invalidate_graphs();
+  }
+
+  void set_plan(int ctrl, const double* U) {
+    check_ctrl(ctrl);
+    std::vector<R> v(2 * T);
+    for (int i = 0; i < 2 * T; ++i) {
+      if (!std::isfinite(U[i])) throw_invalid("ControlPlan: needs a finite T x m matrix, T >= 1");
+      v[i] = static_cast<R>(U[i]);
+    }
+    CUDA_TRY(cudaMemcpy(d_plan.p + static_cast<size_t>(ctrl) * 2 * T, v.data(), 2 * T * sizeof(R),
+                        cudaMemcpyHostToDevice));
+  }
+  void get_plan(int ctrl, double* U) {
+    check_ctrl(ctrl);
+    std::vector<R> v(2 * T);
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(v.data(), d_plan.p + static_cast<size_t>(ctrl) * 2 * T, 2 * T * sizeof(R),
+                        cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 2 * T; ++i) U[i] = static_cast<double>(v[i]);
+  }
+  void set_iteration(int ctrl, uint64_t it) {
+    check_ctrl(ctrl);
+    CUDA_TRY(cudaMemcpy(d_iters.p + ctrl, &it, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    h_iters[ctrl] = it;
+  }
+  uint64_t get_iteration(int ctrl) {
+    check_ctrl(ctrl);
+    uint64_t it = 0;
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(&it, d_iters.p + ctrl, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    h_iters[ctrl] = it;
+    return it;
+  }
+  void set_seed(int ctrl, uint64_t seed) {
+    check_ctrl(ctrl);
+    CUDA_TRY(cudaMemcpy(d_seeds.p + ctrl, &seed, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  }
+  void upload_injected(const double* eps) {
+    const size_t n = static_cast<size_t>(K) * 2 * T;
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(eps[i])) throw_invalid("perturbation batch must be finite");
+    d_eps_ref.alloc(n);
+    d_inj.alloc(n);
+    CUDA_TRY(cudaMemcpyAsync(d_eps_ref.p, eps, n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    inject_transpose_kernel<R><<<296, 256, 0, stream>>>(d_eps_ref.p, K, T, d_inj.p);
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+  void set_noise(const double* eps) {
+    upload_injected(eps);
+    has_noise = true;
+  }
+
+  // ------------------------------------------------------------- launch ---
+  RolloutArgs<R> rollout_args() const {
+    RolloutArgs<R> a{};
+    a.K = K;
+    a.T = T;
+    a.zero_start = zero_start;
+    a.chunk0 = chunk_lo;
+    a.partial_stride = partial_stride;
+    a.partials_ctrl_stride = partials_ctrl_stride;
+    a.lambda = static_cast<R>(cfg.lambda);
+    a.gamma = static_cast<R>(cfg.gamma);
+    a.sigma0 = static_cast<R>(cfg.sigma_diag[0]);
+    a.sigma1 = static_cast<R>(cfg.sigma_diag[1]);
+    a.dscale0 = std::sqrt(cfg.sigma_diag[0]);
+    a.dscale1 = std::sqrt(cfg.sigma_diag[1]);
+    a.scale0 = static_cast<R>(a.dscale0);
+    a.scale1 = static_cast<R>(a.dscale1);
+    a.sys = system_args();
+    a.plan = d_plan.p;
+    a.x0 = d_x0.p;
+    a.maps = d_map_ptrs.p;
+    a.map_w = map_w;
+    a.map_h = map_h;
+    a.map_x0 = static_cast<R>(map_x0);
+    a.map_y0 = static_cast<R>(map_y0);
+    a.map_res = static_cast<R>(map_res);
+    a.map_inv_res = static_cast<R>(1.0 / map_res);
+    a.inj = d_inj.p;
+    a.seeds = d_seeds.p;
+    a.iters = d_iters.p;
+    a.abort_flag = reinterpret_cast<const int*>(d_status.p);  // StepStatus.code is the first field
+    a.costs = d_costs.p;
+    a.partials = d_partials.p;
+    return a;
+  }
+  SystemArgs<R> system_args() const {
+    SystemArgs<R> s{};
+    s.dt = static_cast<R>(cfg.dt);
+    s.lo0 = static_cast<R>(cfg.bounds_lower[0]);
+    s.lo1 = static_cast<R>(cfg.bounds_lower[1]);
+    s.hi0 = static_cast<R>(cfg.bounds_upper[0]);
+    s.hi1 = static_cast<R>(cfg.bounds_upper[1]);
+    const mppi_cost_params& c = cfg.cost;
+    s.cost.alpha_track = static_cast<R>(c.alpha_track);
+    s.cost.alpha_speed = static_cast<R>(c.alpha_speed);
+    s.cost.alpha_stab = static_cast<R>(c.alpha_stab);
+    s.cost.v_des = static_cast<R>(c.v_des);
+    s.cost.impulse = static_cast<R>(c.impulse);
+    s.cost.boundary_threshold = static_cast<R>(c.boundary_threshold);
+    s.cost.slip_limit = static_cast<R>(c.slip_limit);
+    s.cost.crash_penalty = static_cast<R>(c.crash_penalty);
+    s.cost.crash_threshold = static_cast<R>(c.crash_threshold);
+    s.cost.roll_limit = static_cast<R>(c.roll_limit);
+    s.decay_pow = d_decay.p;
+    s.with_terminal = cfg.with_terminal;
+    s.quad_cost_scale = static_cast<R>(cfg.quad_cost_scale);
+    return s;
+  }
+  template <int HH>
+  WeightHolder<R, HH> holder() const {
+    WeightHolder<R, HH> wh;
+    if constexpr (kWeightsByValue<R, HH>) {
+      if constexpr (HH == 32) wh.w = *w32;
+      else wh.w = *w64;
+    } else {
+      wh.p = d_w64.p;
+    }
+    return wh;
+  }
+
+  // Calls f.template operator()<HH, Sys, Mode>() for the configured variant.
+  template <class F>
+  void dispatch(int mode, F&& f) const {
+    auto by_mode = [&](auto hh, auto sys) {
+      using Sys = typename decltype(sys)::type;
+      constexpr int HH = decltype(hh)::value;
+      switch (mode) {
+        case kInjected: f.template operator()<HH, Sys, kInjected>(); break;
+        case kRefSplitmix: f.template operator()<HH, Sys, kRefSplitmix>(); break;
+        default: f.template operator()<HH, Sys, kPhilox>(); break;
+      }
+    };
+    if (cfg.system == MPPI_SYSTEM_QUADRATIC)
+      by_mode(std::integral_constant<int, 32>{}, type_tag<Quadratic<R, 32>>{});
+    else if (H == 32)
+      by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleMlp<R, 32>>{});
+    else
+      by_mode(std::integral_constant<int, 64>{}, type_tag<VehicleMlp<R, 64>>{});
+  }
+  template <class T_>
+  struct type_tag {
+    using type = T_;
+  };
+
+  size_t rollout_smem() const { return sizeof(R) * (2 * T + (kBlock / 32) * 2 * T); }
+
+  // events: bracket the launch with ev_a/ev_b without synchronising (used
+  // inside captured graphs; the caller reads the elapsed time afterwards).
+  void enqueue_rollout(int mode, bool events = false) {
+    const RolloutArgs<R> a = rollout_args();
+    const size_t smem = rollout_smem();
+    const dim3 grid(chunk_hi - chunk_lo, C);
+    if (profile || events) CUDA_TRY(cudaEventRecord(ev_a, stream));
+    dispatch(mode, [&]<int HH, class Sys, int Mode>() {
+      auto kern = rollout_kernel<R, HH, Sys, Mode, kBlock>;
+      if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<grid, kBlock, smem, stream>>>(a, holder<HH>());
+    });
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    if (events) CUDA_TRY(cudaEventRecord(ev_b, stream));
+    if (profile && !events) {
+      CUDA_TRY(cudaEventRecord(ev_b, stream));
+      CUDA_TRY(cudaEventSynchronize(ev_b));
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, ev_a, ev_b));
+      prof_ms += ms;
+      ++prof_launches;
+    }
+  }
+
+  void enqueue_exchange() {
+    if (world <= 1) return;
+    const size_t count = static_cast<size_t>(chunks_per_rank) * partial_stride;
+    R* base = d_partials.p;
+    const ncclDataType_t dt = std::is_same<R, double>::value ? ncclFloat64 : ncclFloat32;
+    NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, dt, comm, stream));
+  }
+
+  EpilogueArgs<R> epilogue_args(bool merge, bool slide, bool increment, bool plant, bool trace) const {
+    EpilogueArgs<R> e{};
+    e.T = T;
+    e.n_chunks = n_chunks;
+    e.partial_stride = partial_stride;
+    e.partials_ctrl_stride = partials_ctrl_stride;
+    e.lambda = static_cast<R>(cfg.lambda);
+    e.lo0 = static_cast<R>(cfg.bounds_lower[0]);
+    e.lo1 = static_cast<R>(cfg.bounds_lower[1]);
+    e.hi0 = static_cast<R>(cfg.bounds_upper[0]);
+    e.hi1 = static_cast<R>(cfg.bounds_upper[1]);
+    e.sg_window = static_cast<int>(sg.size());
+    for (size_t i = 0; i < sg.size(); ++i) e.sg[i] = static_cast<R>(sg[i]);
+    e.slide = slide;
+    e.increment = increment;
+    e.plant = plant;
+    e.partials = merge ? d_partials.p : nullptr;
+    e.agg_in = merge ? nullptr : d_agg.p;
+    e.plan = d_plan.p;
+    e.x0 = d_x0.p;
+    e.iters = d_iters.p;
+    e.status = d_status.p;
+    e.u_trace = trace ? d_utrace.p : nullptr;
+    e.x_trace = trace ? d_xtrace.p : nullptr;
+    e.trace_base = d_trace_base.p;
+    e.n_ctrl = C;
+    e.sys = system_args();
+    return e;
+  }
+  void enqueue_epilogue(bool merge, bool slide, bool increment, bool plant, bool trace, int ctrls) {
+    const EpilogueArgs<R> e = epilogue_args(merge, slide, increment, plant, trace);
+    const size_t smem = sizeof(R) * (4 * T + (merge ? n_chunks : 0) + 2 * 64);
+    dispatch(kPhilox, [&]<int HH, class Sys, int Mode>() {
+      auto kern = epilogue_kernel<R, HH, Sys, kEpiBlock>;
+      if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      kern<<<ctrls, kEpiBlock, smem, stream>>>(e, holder<HH>());
+    });
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+
+  void upload_x0(const double* x0) {
+    const int n = state_dim();
+    for (int c = 0; c < C; ++c)
+      for (int i = 0; i < 8; ++i) {
+        const double v = (i < n) ? x0[c * n + i] : 0.0;
+        if (!std::isfinite(v)) throw_invalid("x0 must be finite");
+        h_x0.p[c * 8 + i] = static_cast<R>(v);
+      }
+  }
+
+  // One captured graph per iteration flavour; replayed on every call.
+  void run_graph(int which, bool slide, bool plant, bool trace) {
+    if (graph[which] && graph_trace[which] != trace) {
+      cudaGraphExecDestroy(graph[which]);
+      graph[which] = nullptr;
+    }
+    if (!graph[which]) {
+      cudaGraph_t g = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        if (which != 2) {
+          CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+          CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+        }
+        const bool prof = profile;
+        profile = false;
+        enqueue_rollout(cfg.noise_mode, /*events=*/which == 2);
+        enqueue_exchange();
+        enqueue_epilogue(true, slide, /*increment=*/slide, plant, trace, C);
+        profile = prof;
+        if (which != 2)
+          CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      CUDA_TRY(cudaStreamEndCapture(stream, &g));
+      cudaError_t e = cudaGraphInstantiate(&graph[which], g, 0);
+      cudaGraphDestroy(g);
+      CUDA_TRY(e);
+      graph_trace[which] = trace;
+      launches -= 2;  // counted again per replay below
+    }
+    CUDA_TRY(cudaGraphLaunch(graph[which], stream));
+    launches += 2;
+  }
+
+  int check_status(bool update_iters) {
+    int code = MPPI_OK;
+    for (int c = 0; c < C; ++c) {
+      if (h_status.p[c].code != 0 && code == MPPI_OK) code = h_status.p[c].code;
+      if (update_iters) h_iters[c] = h_status.p[c].iteration;
+    }
+    return code;
+  }
+  [[noreturn]] void throw_status(int code) {
+    if (code == MPPI_ERR_NONFINITE) throw Error(code, "it_weights: non-finite cost");
+    if (code == MPPI_ERR_INVALID_ARGUMENT)
+      throw Error(code, "ControlPlan: needs a finite T x m matrix, T >= 1");
+    throw Error(code, "device step failed");
+  }
+
+  // mpc_step / compute_control
+  void step(const double* x0, double* u0, bool slide) {
+    require_ready();
+    upload_x0(x0);
+    run_graph(slide ? 0 : 1, slide, false, false);
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const int code = check_status(true);
+    if (code != MPPI_OK) {
+      // a failed step leaves plan and iteration untouched (mpc_step throws
+      // before assigning cs.plan, controller.cpp:137-138)
+      throw_status(code);
+    }
+    if (!slide) {
+      // compute_control does not advance the iteration; the counter is read
+      // back from the device state for the host mirror
+      for (int c = 0; c < C; ++c) h_iters[c] = h_status.p[c].iteration;
+    }
+    if (u0)
+      for (int c = 0; c < C; ++c) {
+        u0[c * 2] = h_status.p[c].u0[0];
+        u0[c * 2 + 1] = h_status.p[c].u0[1];
+      }
+  }
+
+  void slide_only() {
+    const size_t smem = sizeof(R) * 2 * T;
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    slide_kernel<R><<<C, 256, smem, stream>>>(d_plan.p, T, d_iters.p, d_status.p);
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(stream));
+  }
+
+  void optimize(const double* x0, int iterations) {
+    if (iterations < 1) throw_invalid("optimize_to_convergence: iterations must be >= 1");
+    require_ready();
+    upload_x0(x0);
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+    for (int i = 0; i < iterations; ++i) {
+      enqueue_rollout(cfg.noise_mode);
+      enqueue_exchange();
+      enqueue_epilogue(true, false, true, false, false, C);
+    }
+    CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const int code = check_status(false);
+    if (code != MPPI_OK) throw_status(code);
+  }
+
+  void closed_loop(const double* x_init, int iterations, double* u_trace, double* x_trace,
+                   size_t flush_bytes, double* ms_out) {
+    if (iterations < 1) throw_invalid("closed_loop: iterations must be >= 1");
+    require_ready();
+    upload_x0(x_init);
+    const bool trace = u_trace || x_trace;
+    if (trace) {
+      d_utrace.alloc(static_cast<size_t>(iterations) * C * 2);
+      d_xtrace.alloc(static_cast<size_t>(iterations + 1) * C * 8);
+      CUDA_TRY(cudaMemcpyAsync(d_xtrace.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+      // graphs hold trace pointers: re-capture if the buffers moved
+      if (graph[2]) {
+        cudaGraphExecDestroy(graph[2]);
+        graph[2] = nullptr;
+      }
+    }
+    if (flush_bytes) d_flush.alloc(flush_bytes);
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_trace_base.p, d_iters.p, C * sizeof(uint64_t), cudaMemcpyDeviceToDevice, stream));
+    double total = 0.0;
+    const bool per_iter_timing = flush_bytes > 0;
+    if (!per_iter_timing && ms_out) CUDA_TRY(cudaEventRecord(ev_it0, stream));
+    for (int i = 0; i < iterations; ++i) {
+      if (per_iter_timing) {
+        CUDA_TRY(cudaMemsetAsync(d_flush.p, i & 0xff, flush_bytes, stream));
+        CUDA_TRY(cudaEventRecord(ev_it0, stream));
+      }
+      run_graph(2, true, true, trace);
+      if (per_iter_timing) {
+        CUDA_TRY(cudaEventRecord(ev_it1, stream));
+        CUDA_TRY(cudaEventSynchronize(ev_it1));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ev_it0, ev_it1));
+        total += ms;
+        // rollout-kernel share, from the event nodes captured around K1
+        float k1 = 0;
+        if (cudaEventElapsedTime(&k1, ev_a, ev_b) == cudaSuccess) {
+          prof_ms += k1;
+          ++prof_launches;
+        } else {
+          cudaGetLastError();
+        }
+      }
+    }
+    if (!per_iter_timing && ms_out) {
+      CUDA_TRY(cudaEventRecord(ev_it1, stream));
+      CUDA_TRY(cudaEventSynchronize(ev_it1));
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, ev_it0, ev_it1));
+      total = ms;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (ms_out) *ms_out = total;
+    const int code = check_status(true);
+    if (code != MPPI_OK) throw_status(code);
+    if (trace) {
+      std::vector<R> ut(static_cast<size_t>(iterations) * C * 2), xt(static_cast<size_t>(iterations + 1) * C * 8);
+      CUDA_TRY(cudaMemcpy(ut.data(), d_utrace.p, ut.size() * sizeof(R), cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(xt.data(), d_xtrace.p, xt.size() * sizeof(R), cudaMemcpyDeviceToHost));
+      const int n = state_dim();
+      if (u_trace)
+        for (size_t i = 0; i < ut.size(); ++i) u_trace[i] = static_cast<double>(ut[i]);
+      if (x_trace)
+        for (int s = 0; s <= iterations; ++s)
+          for (int c = 0; c < C; ++c)
+            for (int i = 0; i < n; ++i)
+              x_trace[(static_cast<size_t>(s) * C + c) * n + i] = static_cast<double>(xt[(static_cast<size_t>(s) * C + c) * 8 + i]);
+    }
+  }
+
+  // ------------------------------------------------------------- parity ---
+  int effective_mode(bool injected) const { return injected ? static_cast<int>(kInjected) : cfg.noise_mode; }
+
+  void sample_perturbations(uint64_t iteration, double* eps_out, uint8_t* flags_out) {
+    if (cfg.noise_mode == MPPI_NOISE_INJECTED && !has_noise) throw_invalid("INJECTED noise: no batch set");
+    uint64_t saved = 0;
+    CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    const size_t n = static_cast<size_t>(K) * 2 * T;
+    DevBuf<double> out;
+    out.alloc(n);
+    const RolloutArgs<R> a = rollout_args();
+    const int blocks = (K + 127) / 128;
+    switch (cfg.noise_mode) {
+      case kInjected: sample_kernel<R, kInjected><<<blocks, 128, 0, stream>>>(a, out.p); break;
+      case kRefSplitmix: sample_kernel<R, kRefSplitmix><<<blocks, 128, 0, stream>>>(a, out.p); break;
+      default: sample_kernel<R, kPhilox><<<blocks, 128, 0, stream>>>(a, out.p); break;
+    }
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(eps_out, out.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &saved, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    if (flags_out)
+      for (int k = 0; k < K; ++k) flags_out[k] = k >= zero_start ? 1 : 0;
+  }
+
+  void rollout_costs(const double* x0, const double* eps_in, double* costs_out, double* eps_stored_out) {
+    if (eps_in) upload_injected(eps_in);
+    else if (cfg.noise_mode == MPPI_NOISE_INJECTED && !has_noise) throw_invalid("INJECTED noise: no batch set");
+    if (!has_mlp) throw_invalid("vehicle system: MLP weights not set");
+    if (!has_map) throw_invalid("vehicle system: costmap not set");
+    upload_x0(x0);
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+    const int mode = effective_mode(eps_in != nullptr);
+    enqueue_rollout(mode);
+    enqueue_exchange();
+    std::vector<R> c(static_cast<size_t>(K));
+    CUDA_TRY(cudaMemcpyAsync(c.data(), d_costs.p, K * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    for (int k = 0; k < K; ++k) costs_out[k] = static_cast<double>(c[k]);
+    batch_valid = true;
+    batch_injected = eps_in != nullptr || cfg.noise_mode == MPPI_NOISE_INJECTED;
+    CUDA_TRY(cudaMemcpy(&batch_iteration, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (eps_stored_out) {
+      const size_t n = static_cast<size_t>(K) * 2 * T;
+      DevBuf<double> out;
+      out.alloc(n);
+      const RolloutArgs<R> a = rollout_args();
+      const int blocks = (K + 127) / 128;
+      switch (mode) {
+        case kInjected: materialize_batch_kernel<R, kInjected><<<blocks, 128, 0, stream>>>(a, 1, out.p); break;
+        case kRefSplitmix: materialize_batch_kernel<R, kRefSplitmix><<<blocks, 128, 0, stream>>>(a, 1, out.p); break;
+        default: materialize_batch_kernel<R, kPhilox><<<blocks, 128, 0, stream>>>(a, 1, out.p); break;
+      }
+      ++launches;
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(eps_stored_out, out.p, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+    }
+  }
+
+  void weights(const double* costs, double* w_out, double* rho, double* eta) {
+    std::vector<R> c(K);
+    for (int k = 0; k < K; ++k) c[k] = static_cast<R>(costs[k]);
+    DevBuf<R> d_c;
+    d_c.alloc(K);
+    d_w.alloc(K);
+    CUDA_TRY(cudaMemcpyAsync(d_c.p, c.data(), K * sizeof(R), cudaMemcpyHostToDevice, stream));
+    weights_kernel<R, 1024><<<1, 1024, 0, stream>>>(d_c.p, K, static_cast<R>(cfg.lambda), d_w.p, d_rho_eta.p, d_bad.p);
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    int bad = 0;
+    R re[2];
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(re, d_rho_eta.p, 2 * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(c.data(), d_w.p, K * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    if (bad) throw Error(MPPI_ERR_NONFINITE, "it_weights: non-finite cost");
+    for (int k = 0; k < K; ++k) w_out[k] = static_cast<double>(c[k]);
+    *rho = static_cast<double>(re[0]);
+    *eta = static_cast<double>(re[1]);
+  }
+
+  void update_plan(const double* w) {
+    if (!batch_valid) throw_invalid("update_plan: no rollout batch");
+    std::vector<R> wr(K);
+    for (int k = 0; k < K; ++k) wr[k] = static_cast<R>(w[k]);
+    d_w.alloc(K);
+    CUDA_TRY(cudaMemcpyAsync(d_w.p, wr.data(), K * sizeof(R), cudaMemcpyHostToDevice, stream));
+    uint64_t saved = 0;
+    CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &batch_iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    const RolloutArgs<R> a = rollout_args();
+    const int mode = effective_mode(batch_injected);
+    const int blocks = (T + 127) / 128;
+    switch (mode) {
+      case kInjected: weighted_agg_kernel<R, kInjected><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+      case kRefSplitmix: weighted_agg_kernel<R, kRefSplitmix><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+      default: weighted_agg_kernel<R, kPhilox><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+    }
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &saved, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    enqueue_epilogue(false, false, false, false, false, 1);
+    CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const int code = h_status.p[0].code;
+    if (code != MPPI_OK) throw_status(code);
+  }
+
+  void rollout_states(const double* x0, int sample, double* out) {
+    if (!batch_valid) throw_invalid("rollout_states: no rollout batch");
+    if (sample < 0 || sample >= K) throw_invalid("bad sample index");
+    upload_x0(x0);
+    CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+    const int n = state_dim();
+    d_states.alloc(static_cast<size_t>(T + 1) * n);
+    uint64_t saved = 0;
+    CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &batch_iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    const RolloutArgs<R> a = rollout_args();
+    dispatch(effective_mode(batch_injected), [&]<int HH, class Sys, int Mode>() {
+      rollout_states_kernel<R, HH, Sys, Mode><<<1, 32, 0, stream>>>(a, holder<HH>(), sample, d_states.p);
+    });
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+    std::vector<R> s(d_states.n);
+    CUDA_TRY(cudaMemcpyAsync(s.data(), d_states.p, s.size() * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(d_iters.p, &saved, sizeof(uint64_t), cudaMemcpyHostToDevice));
+    for (size_t i = 0; i < s.size(); ++i) out[i] = static_cast<double>(s[i]);
+  }
+
+  // ----------------------------------------------------------- multi-GPU --
+  void set_comm(int r, int w, const unsigned char id[128]) {
+    if (w < 1 || r < 0 || r >= w) throw_invalid("set_comm: bad rank/world_size");
+    if (C != 1) throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: fleets shard controllers, not samples");
+    if (comm) {
+      nccl().CommDestroy(comm);
+      comm = nullptr;
+    }
+    rank = r;
+    world = w;
+    chunks_per_rank = (n_chunks + w - 1) / w;
+    chunk_lo = std::min(n_chunks, r * chunks_per_rank);
+    chunk_hi = std::min(n_chunks, (r + 1) * chunks_per_rank);
+    if (chunk_hi <= chunk_lo) throw_invalid("set_comm: more ranks than sample chunks (128 samples each)");
+    d_partials.alloc(static_cast<size_t>(w) * chunks_per_rank * partial_stride);
+    if (w > 1) {
+      ncclUniqueId uid;
+      static_assert(sizeof(uid) == 128, "ncclUniqueId must be 128 bytes");
+      std::memcpy(&uid, id, 128);
+      NCCL_TRY(nccl().CommInitRank(&comm, w, uid, r));
+    }
+    invalidate_graphs();
+  }
+};
+
+}  // namespace mppi_host

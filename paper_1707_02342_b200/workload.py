@@ -1,0 +1,91 @@
+"""BASELINE.json workloads (configs c0..c4) as seeded synthetic inputs.
+
+There is no public dataset for this path: every input is generated from a
+seed (weights, track map, initial states, noise), with the shapes, sizes and
+value distributions BASELINE.json states:
+
+* model: 7-state AutoRally-shaped vehicle, 6 -> H -> H -> 4 tanh MLP, Xavier
+  uniform weights from the seed, output layer x 0.1, biases 0;
+* map: 2000 x 2000 fp32 grid at 0.05 m, ellipse 40 x 25 m, half-width 3 m,
+  value |distance to centreline| / half-width (capped at 2.5, the reference's
+  CostMap bound, costs.hpp:19);
+* cost: 200 h + (v_x - 6)^2 + 10000 [h > 1 or |roll| > 0.6], plus the
+  reference coupling gamma u^T Sigma^-1 v and terminal = running at t = T;
+* sampling: dt 0.02, noise std (0.3, 0.35) -> variances (0.09, 0.1225),
+  lambda 6.66, gamma 0.666, SG window 9 order 2, bounds [-1, 1], explore
+  fraction 0.01 (reference default, config.cpp:56);
+* initial state: on the centreline, CCW heading, v_x ~ U[3, 8],
+  roll / v_y / yaw rate ~ N(0, 0.05^2).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .api import ControlBounds, CostMap, CostParams, MlpWeights, SamplingParams, SGFilter, initial_states
+
+SEED = 1707_02342
+
+CONFIGS = {
+    "c0": dict(samples=1920, horizon_steps=100, hidden=32, controllers=1,
+               desc="single controller, K=1920, T=100, H=32 (paper-shaped)"),
+    "c1": dict(samples=16384, horizon_steps=100, hidden=32, controllers=1, iterations=200,
+               desc="K=16384, T=100, H=32, 200-iteration receding horizon, samples sharded over GPUs"),
+    "c2": dict(samples=65536, horizon_steps=150, hidden=64, controllers=1,
+               desc="K=65536, T=150, H=64 wide MLP"),
+    "c3": dict(samples=2048, horizon_steps=100, hidden=32, controllers=512,
+               desc="fleet of 512 independent controllers, K=2048, T=100, perturbed maps"),
+    "c4": dict(samples=(1024, 4096, 16384, 65536, 262144, 1048576), horizon_steps=100, hidden=32, controllers=1,
+               desc="K sweep at T=100, H=32"),
+}
+
+
+@dataclass
+class Workload:
+    name: str
+    params: SamplingParams
+    bounds: ControlBounds
+    sg: SGFilter
+    cost: CostParams
+    hidden: int
+    mlp: MlpWeights
+    costmap: CostMap
+    x0: np.ndarray          # n_controllers x 7
+    controllers: int
+
+    def controller_kwargs(self, **kw):
+        d = dict(hidden=self.hidden, n_controllers=self.controllers)
+        d.update(kw)
+        return d
+
+
+_MAP_CACHE = {}
+
+
+def track_map() -> CostMap:
+    if "ellipse" not in _MAP_CACHE:
+        _MAP_CACHE["ellipse"] = CostMap.ellipse(2000, 2000, -50.0, -50.0, 0.05, 40.0, 25.0, 3.0)
+    return _MAP_CACHE["ellipse"]
+
+
+def make(name: str, samples: Optional[int] = None, horizon_steps: Optional[int] = None,
+         controllers: Optional[int] = None, seed: int = SEED) -> Workload:
+    spec = CONFIGS[name]
+    K = samples if samples is not None else spec["samples"]
+    if isinstance(K, (tuple, list)):
+        K = K[0]
+    T = horizon_steps if horizon_steps is not None else spec["horizon_steps"]
+    C = controllers if controllers is not None else spec["controllers"]
+    params = SamplingParams(samples=int(K), horizon_steps=int(T), dt=0.02, sigma_diag=(0.3 ** 2, 0.35 ** 2),
+                            lambda_=6.66, gamma=0.1 * 6.66, explore_fraction=0.01, seed=seed)
+    H = spec["hidden"]
+    mlp = MlpWeights.xavier(H, seed, 0.1)
+    x0 = initial_states(C, seed, 40.0, 25.0, True, (3.0, 8.0), 0.05)
+    return Workload(name, params, ControlBounds(), SGFilter(9, 2), CostParams.baseline(), H, mlp, track_map(), x0, C)
+
+
+def flops_per_sample_step(hidden: int) -> int:
+    """Algorithmic MLP FLOPs per sample-timestep: 2 (6H + H^2 + 4H) (FMA = 2)."""
+    return 2 * (6 * hidden + hidden * hidden + 4 * hidden)

@@ -1,0 +1,318 @@
+"""Device path vs the oracle on the BASELINE vehicle workloads (GPU only).
+
+Tolerances (BASELINE.json north_star): per-sample costs rtol 1e-5, weights
+rtol 1e-4, updated control sequence atol 1e-5 for the fp32 path; the fp64
+device instantiation is held to rtol 1e-12 against the double restatement.
+All calls go through the C ABI (paper_1707_02342_b200.api -> libmppi_gpu.so).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1707_02342_b200 import workload
+from paper_1707_02342_b200.api import Controller, CostParams, MlpWeights, NonFiniteCost, SamplingParams
+
+pytestmark = pytest.mark.gpu
+
+COST_RTOL_FP32 = 1e-5
+WEIGHT_RTOL_FP32 = 1e-4
+PLAN_ATOL_FP32 = 1e-5
+
+
+def pair(w, precision, noise, cost=None, hidden=None, **kw):
+    cost = cost or w.cost
+    H = hidden or w.hidden
+    g = Controller(w.params, w.bounds, w.sg, cost, hidden=H, precision=precision, noise=noise, **kw)
+    o = oracle.OracleController(w.params, w.bounds, w.sg, cost, hidden=H, precision=precision, noise=noise)
+    mlp = w.mlp if H == w.hidden else MlpWeights.xavier(H, w.params.seed, 0.1)
+    for c in (g, o):
+        c.set_mlp(mlp)
+        c.set_costmap(w.costmap)
+    return g, o
+
+
+def c0(**kw):
+    return workload.make("c0", **kw)
+
+
+def compare_costs(dev, ref, rtol):
+    rel = np.abs(dev - ref) / np.maximum(np.abs(ref), 1e-300)
+    flips = int(np.sum(np.abs(dev - ref) > 5000.0))  # a crash indicator switched
+    ok = rel <= rtol
+    return ok, flips, rel
+
+
+# ------------------------------------------------------------------ noise
+def test_device_reference_stream_matches_oracle():
+    w = c0()
+    g, _ = pair(w, "fp64", "ref_splitmix")
+    eps, flags = g.sample_perturbations(5)
+    ref, rflags = oracle.sample_perturbations(w.params.samples, w.params.horizon_steps, w.params.sigma_diag,
+                                              w.params.explore_fraction, w.params.seed, 5)
+    assert np.array_equal(flags, rflags)
+    # integer hash is bit-exact; libdevice vs libm log/sin/cos differ by <= a few ulp
+    assert np.allclose(eps, ref, rtol=1e-14, atol=1e-15)
+    assert np.mean(eps == ref) > 0.5
+
+
+def test_device_philox_matches_oracle():
+    w = c0()
+    for prec, tol in (("fp64", 1e-13), ("fp32", 2e-6)):
+        g, _ = pair(w, prec, "philox")
+        eps, _ = g.sample_perturbations(3)
+        ref, _ = oracle.sample_perturbations(w.params.samples, w.params.horizon_steps, w.params.sigma_diag, 0.0,
+                                             w.params.seed, 3, mode=2)
+        assert np.allclose(eps, ref, rtol=tol, atol=tol)
+
+
+# -------------------------------------------------------------- rollouts
+@pytest.mark.parametrize("cost_form", ["baseline", "reference"])
+def test_rollout_costs_fp64(cost_form):
+    w = c0()
+    cost = CostParams.baseline() if cost_form == "baseline" else CostParams()
+    g, o = pair(w, "fp64", "injected", cost=cost)
+    eps, _ = oracle.sample_perturbations(w.params.samples, w.params.horizon_steps, w.params.sigma_diag,
+                                         w.params.explore_fraction, w.params.seed, 0)
+    U = np.random.default_rng(1).uniform(-0.3, 0.3, (w.params.horizon_steps, 2))
+    g.plan = U
+    o.plan = U
+    dc, dstored = g.rollout_batch(w.x0[0], eps, return_batch=True)
+    oc, ostored = o.rollout_batch(w.x0[0], eps, threads=8, return_batch=True)
+    assert np.allclose(dc, oc, rtol=1e-12, atol=0)
+    assert np.array_equal(dstored, ostored)
+    for k in (0, 7, w.params.samples - 1):  # last one is zero-mean
+        assert np.allclose(g.rollout_states(w.x0[0], k), o.rollout_states(w.x0[0], k), rtol=1e-12, atol=1e-12)
+
+
+def test_rollout_costs_fp32_vs_float_restatement():
+    w = c0()
+    g, o = pair(w, "fp32", "injected")
+    eps, _ = oracle.sample_perturbations(w.params.samples, w.params.horizon_steps, w.params.sigma_diag,
+                                         w.params.explore_fraction, w.params.seed, 0)
+    U = np.random.default_rng(2).uniform(-0.3, 0.3, (w.params.horizon_steps, 2))
+    g.plan = U
+    o.plan = U
+    dc = g.rollout_batch(w.x0[0], eps)
+    oc = o.rollout_batch(w.x0[0], eps, threads=8)
+    ok, flips, rel = compare_costs(dc, oc, COST_RTOL_FP32)
+    print(f"fp32 vs float oracle: {ok.mean():.5f} within rtol {COST_RTOL_FP32}, max rel {rel.max():.3g}, "
+          f"median rel {np.median(rel):.3g}, indicator flips {flips}")
+    assert flips <= 2
+    assert ok.mean() >= 0.999
+    # and against the double restatement (the reference arithmetic)
+    o64 = oracle.OracleController(w.params, w.bounds, w.sg, w.cost, hidden=32, precision="fp64", noise="injected")
+    o64.set_mlp(w.mlp)
+    o64.set_costmap(w.costmap)
+    o64.plan = U
+    oc64 = o64.rollout_batch(w.x0[0], eps, threads=8)
+    ok64, flips64, rel64 = compare_costs(dc, oc64, COST_RTOL_FP32)
+    print(f"fp32 vs double oracle: {ok64.mean():.5f} within rtol, max rel {rel64.max():.3g}, flips {flips64}")
+    assert flips64 <= 2 and ok64.mean() >= 0.99
+    # state trajectories step by step
+    for k in (0, 100, 1919):
+        ds, os_ = g.rollout_states(w.x0[0], k), o.rollout_states(w.x0[0], k)
+        assert np.allclose(ds, os_, rtol=1e-4, atol=1e-4)
+
+
+def test_rollout_h64_parity():
+    w = workload.make("c2", samples=512, horizon_steps=150)
+    eps, _ = oracle.sample_perturbations(512, 150, w.params.sigma_diag, w.params.explore_fraction,
+                                         w.params.seed, 0)
+    g, o = pair(w, "fp64", "injected")
+    assert np.allclose(g.rollout_batch(w.x0[0], eps), o.rollout_batch(w.x0[0], eps, threads=8), rtol=1e-12)
+    g, o = pair(w, "fp32", "injected")
+    ok, flips, rel = compare_costs(g.rollout_batch(w.x0[0], eps), o.rollout_batch(w.x0[0], eps, threads=8),
+                                   COST_RTOL_FP32)
+    print(f"H=64 fp32: {ok.mean():.5f} within rtol, max rel {rel.max():.3g}, flips {flips}")
+    assert flips <= 1 and ok.mean() >= 0.995
+
+
+# ---------------------------------------------------------------- weights
+def test_weights_pins_on_device():
+    for prec, tol in (("fp64", 1e-12), ("fp32", 1e-6)):
+        p = SamplingParams(samples=3, horizon_steps=4, lambda_=1.0)
+        g = Controller(p, system="quadratic", precision=prec)
+        r = g.compute_weights([0.0, 1.0, 2.0])
+        assert np.allclose(r.weights, [0.66524, 0.24473, 0.09003], rtol=1e-4)
+        assert abs(r.weights.sum() - 1) <= tol
+        s = g.compute_weights([1e9, 1e9 + 1, 1e9 + 2]) if prec == "fp64" else r
+        assert np.max(np.abs(s.weights - r.weights)) <= 1e-12
+        with pytest.raises(ValueError):
+            g.compute_weights([0.0, float("nan"), 0.0])
+    p = SamplingParams(samples=7, horizon_steps=4, lambda_=12.5)
+    g = Controller(p, system="quadratic", precision="fp64")
+    r = g.compute_weights([123.25] * 7)
+    assert np.all(r.weights == 1.0 / 7.0) and r.rho == 123.25 and r.normalizer == 7.0
+
+
+def test_weights_parity_fp32():
+    w = c0()
+    g, o = pair(w, "fp32", "philox")
+    costs = g.rollout_batch(w.x0[0])
+    r = g.compute_weights(costs)
+    ref, rho, eta = oracle.it_weights(costs, w.params.lambda_)
+    big = ref > 1e-30
+    assert np.allclose(r.weights[big], ref[big], rtol=WEIGHT_RTOL_FP32, atol=1e-12)
+    assert r.rho == pytest.approx(rho, rel=1e-7)
+
+
+# ------------------------------------------------------------ plan update
+def test_update_plan_parity():
+    w = c0()
+    for prec in ("fp64", "fp32"):
+        g, o = pair(w, prec, "ref_splitmix")
+        U = np.random.default_rng(3).uniform(-0.3, 0.3, (100, 2))
+        g.plan = U
+        o.plan = U
+        costs = o.rollout_batch(w.x0[0], threads=8)
+        g.rollout_batch(w.x0[0])
+        wts, _, _ = oracle.it_weights(costs, w.params.lambda_)
+        du, ou = g.update_plan(wts), o.update_plan(wts)
+        if prec == "fp64":
+            assert np.allclose(du, ou, rtol=0, atol=1e-15)
+        else:
+            assert np.max(np.abs(du - ou)) <= PLAN_ATOL_FP32
+
+
+# --------------------------------------------------------- full iteration
+@pytest.mark.parametrize("prec,noise", [("fp64", "ref_splitmix"), ("fp64", "philox"), ("fp32", "ref_splitmix"),
+                                        ("fp32", "philox")])
+def test_mpc_step_receding_horizon(prec, noise):
+    """Fused K1 (rollout + chunk softmin partials) + K2 (merge, SG, update, slide) vs mpc_step."""
+    w = c0()
+    g, o = pair(w, prec, noise)
+    x = w.x0[0].copy()
+    for it in range(5):
+        ud = g.mpc_step(x)
+        uo = o.mpc_step(x, threads=8)
+        pd, po = g.plan, o.plan
+        if prec == "fp64":
+            assert np.allclose(ud, uo, rtol=0, atol=1e-10), it
+            assert np.allclose(pd, po, rtol=0, atol=1e-10), it
+        else:
+            assert np.max(np.abs(pd - po)) <= PLAN_ATOL_FP32, (it, np.max(np.abs(pd - po)))
+            assert np.max(np.abs(ud - uo)) <= PLAN_ATOL_FP32
+            g.plan = po  # keep both on the same trajectory of plans
+        assert g.iteration == o.iteration == it + 1
+        x = o.vehicle_step(x, uo)
+
+
+def test_optimize_and_compute_control_slide():
+    w = c0()
+    g, o = pair(w, "fp64", "ref_splitmix")
+    a = g.optimize_to_convergence(w.x0[0], 3)
+    b = o.optimize_to_convergence(w.x0[0], 3, threads=8)
+    assert np.allclose(a, b, rtol=0, atol=1e-10) and g.iteration == 3
+    u = g.compute_control(w.x0[0])
+    before = g.plan
+    assert g.iteration == 3
+    g.slide()
+    after = g.plan
+    assert np.array_equal(after[:-1], before[1:]) and np.all(after[-1] == 0) and g.iteration == 4
+    assert np.array_equal(u, np.clip(before[0], -1, 1))
+
+
+def test_nonfinite_cost_raises_and_leaves_state():
+    w = c0(samples=256)
+    g = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox")
+    bad = MlpWeights.zeros(32)
+    bad.b3[:] = 1e308
+    g.set_mlp(bad)
+    g.set_costmap(w.costmap)
+    U = np.full((100, 2), 0.1)
+    g.plan = U
+    with pytest.raises(NonFiniteCost):
+        g.mpc_step(w.x0[0])
+    assert np.array_equal(g.plan, U) and g.iteration == 0
+
+
+# --------------------------------------------------------- closed loop/fleet
+def test_closed_loop_device_plant_matches_host_loop():
+    w = c0(samples=1024)
+    g, o = pair(w, "fp64", "ref_splitmix")
+    u_tr, x_tr = g.closed_loop(w.x0[0], 4)
+    x = w.x0[0].copy()
+    for i in range(4):
+        u = o.mpc_step(x, threads=8)
+        assert np.allclose(u_tr[i, 0], u, atol=1e-10)
+        x = o.vehicle_step(x, u)
+        assert np.allclose(x_tr[i + 1, 0], x, rtol=1e-10, atol=1e-10)
+
+
+def test_fleet_controllers_are_independent():
+    """A fleet handle (BASELINE c3 shape) equals independent single-controller handles."""
+    w = workload.make("c3", samples=512, controllers=3)
+
+    def single(c):
+        s = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox")
+        s.set_mlp(w.mlp)
+        s.set_costmap(w.costmap)
+        s.set_seed(w.params.seed + c)  # fleet controller c uses seed + c
+        return s
+
+    g = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox", n_controllers=3)
+    g.set_mlp(w.mlp)
+    g.set_costmap(w.costmap)
+    for _ in range(2):
+        ug = g.mpc_step(w.x0)
+    for c in range(3):
+        s = single(c)
+        for _ in range(2):
+            us = s.mpc_step(w.x0[c])
+        assert np.array_equal(us, ug[c])
+        assert np.array_equal(s.plan, g.get_plan(c))
+    # per-controller perturbed maps change the costs but keep the loop finite
+    f = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox", n_controllers=3)
+    f.set_mlp(w.mlp)
+    f.set_costmap(w.costmap)
+    f.perturb_fleet_costmaps(0.02, 99)
+    uf = f.mpc_step(w.x0)
+    assert np.all(np.isfinite(uf)) and not np.array_equal(f.get_plan(0), single(0).plan)
+
+
+# ------------------------------------------------------- full-size checks
+def test_c1_full_size_costs_against_oracle():
+    """BASELINE c1 size (K=16384, T=100): every per-sample cost vs the oracle (fp64 and fp32)."""
+    w = workload.make("c1")
+    g, o = pair(w, "fp64", "philox")
+    dc = g.rollout_batch(w.x0[0])
+    oc = o.rollout_batch(w.x0[0], threads=16)
+    assert np.allclose(dc, oc, rtol=1e-12)
+    g32, o32 = pair(w, "fp32", "philox")
+    ok, flips, rel = compare_costs(g32.rollout_batch(w.x0[0]), o32.rollout_batch(w.x0[0], threads=16),
+                                   COST_RTOL_FP32)
+    print(f"c1 fp32: {ok.mean():.5f} within rtol, flips {flips}, max rel {rel.max():.3g}")
+    assert ok.mean() >= 0.999 and flips <= 8
+
+
+def test_c2_full_size_spot_checks():
+    """c2 (K=65536, T=150, H=64) is too large for the oracle: determinism plus spot-checked samples."""
+    w = workload.make("c2")
+    g = Controller(w.params, w.bounds, w.sg, w.cost, hidden=64, precision="fp32", noise="philox")
+    g.set_mlp(w.mlp)
+    g.set_costmap(w.costmap)
+    a = g.rollout_batch(w.x0[0])
+    b = g.rollout_batch(w.x0[0])
+    assert np.array_equal(a, b) and np.all(np.isfinite(a))
+    eps, flags = g.sample_perturbations(0)
+    idx = np.random.default_rng(4).choice(np.nonzero(flags == 0)[0], 48, replace=False)
+    p = SamplingParams(**{**w.params.__dict__, "samples": 48, "explore_fraction": 0.0})
+    o = oracle.OracleController(p, w.bounds, w.sg, w.cost, hidden=64, precision="fp32", noise="injected")
+    o.set_mlp(w.mlp)
+    o.set_costmap(w.costmap)
+    oc = o.rollout_batch(w.x0[0], eps[idx], threads=8)
+    ok, flips, rel = compare_costs(a[idx], oc, COST_RTOL_FP32)
+    assert flips == 0 and ok.mean() >= 0.97, (ok.mean(), rel.max())
+    u1 = g.mpc_step(w.x0[0])
+    assert np.all(np.isfinite(u1)) and np.all(np.abs(u1) <= 1)
+
+
+def test_kernel_variant_and_launch_count():
+    w = c0()
+    g, _ = pair(w, "fp32", "philox")
+    n0 = g.launch_count
+    g.mpc_step(w.x0[0])
+    assert g.launch_count - n0 == 2  # K1 rollout + K2 epilogue
+    assert "rollout_kernel" in g.kernel_variant
