@@ -541,8 +541,9 @@ struct Controller {
     return sample_perturbations<R>(p, it, cfg.noise_mode);
   }
 
-  // rollout_batch (controller.cpp:55-109)
-  std::vector<R> rollout_batch(const System<R>& sys, const R* x0, Batch<R>& batch,
+  // rollout_batch (controller.cpp:55-109).  Mixed precision as on the
+  // device: per-step terms in R, the T-term cost sum in double.
+  std::vector<double> rollout_batch(const System<R>& sys, const R* x0, Batch<R>& batch,
                                int n_threads) const {
     p.validate();
     const int K = batch.K, T = p.horizon_steps, m = sys.control_dim;
@@ -553,14 +554,14 @@ struct Controller {
           for (int c = 0; c < m; ++c) batch.at(k, t, c) -= plan[t * m + c];
     const R lambda = static_cast<R>(p.lambda), gamma = static_cast<R>(p.gamma);
     const R sig[2] = {static_cast<R>(p.sigma_diag[0]), static_cast<R>(p.sigma_diag[1])};
-    std::vector<R> costs(K);
+    std::vector<double> costs(K);
     parallel_for_chunks(K, n_threads, [&](int begin, int end) {
       std::vector<R> x(sys.state_dim), xn(sys.state_dim);
       R u[2], v[2];
       for (int k = begin; k < end; ++k) {
         for (int i = 0; i < sys.state_dim; ++i) x[i] = x0[i];
         const bool zero_mean = batch.flags[k] != 0;
-        R cost = 0;
+        double cost = 0;
         for (int t = 0; t < T; ++t) {
           R uv = 0, uu = 0;
           for (int c = 0; c < m; ++c) {
@@ -573,9 +574,9 @@ struct Controller {
           x.swap(xn);
           const R coupling =
               zero_mean ? (gamma - lambda) * uv + R(0.5) * lambda * uu : gamma * uv;
-          cost += sys.running_cost(x.data(), t) + coupling;
+          cost += static_cast<double>(sys.running_cost(x.data(), t) + coupling);
         }
-        cost += sys.terminal_cost(x.data());
+        cost += static_cast<double>(sys.terminal_cost(x.data()));
         costs[k] = cost;
       }
     });
@@ -583,20 +584,22 @@ struct Controller {
   }
 
   // update_plan (controller.cpp:118-131): ascending k, skipping zero weights.
-  std::vector<R> update_plan(const Batch<R>& batch, const std::vector<R>& w) const {
+  // The aggregate and its smoothing are double; U' = U + agg is rounded once
+  // to R (the device does the same).
+  std::vector<R> update_plan(const Batch<R>& batch, const std::vector<double>& w) const {
     const int K = batch.K, T = p.horizon_steps;
     if (static_cast<int>(w.size()) != K)
       throw std::invalid_argument("update_plan: weight/sample count mismatch");
-    std::vector<R> agg(static_cast<size_t>(T) * 2, R(0));
+    std::vector<double> agg(static_cast<size_t>(T) * 2, 0.0);
     for (int k = 0; k < K; ++k) {
-      if (w[k] == R(0)) continue;
+      if (w[k] == 0.0) continue;
       for (int t = 0; t < T; ++t)
-        for (int c = 0; c < 2; ++c) agg[t * 2 + c] += w[k] * batch.at(k, t, c);
+        for (int c = 0; c < 2; ++c) agg[t * 2 + c] += w[k] * static_cast<double>(batch.at(k, t, c));
     }
-    if (!sg_r.empty()) agg = sg_smooth<R>(agg, T, 2, sg_r);
+    if (!sg.empty()) agg = sg_smooth<double>(agg, T, 2, sg);
     std::vector<R> out(plan);
     for (size_t i = 0; i < out.size(); ++i) {
-      out[i] += agg[i];
+      out[i] = static_cast<R>(static_cast<double>(plan[i]) + agg[i]);
       if (!std::isfinite(out[i]))
         throw std::invalid_argument("ControlPlan: needs a finite T x m matrix, T >= 1");
     }
@@ -607,8 +610,8 @@ struct Controller {
   void mpc_step(const R* x0, R u0[2], int n_threads) {
     const System<R> sys = system();
     Batch<R> batch = sample(iteration);
-    const std::vector<R> costs = rollout_batch(sys, x0, batch, n_threads);
-    const Weights<R> w = it_weights(costs, static_cast<R>(p.lambda));
+    const std::vector<double> costs = rollout_batch(sys, x0, batch, n_threads);
+    const Weights<double> w = it_weights<double>(costs, p.lambda);
     plan = update_plan(batch, w.w);
     for (int c = 0; c < 2; ++c) u0[c] = clampv(plan[c], lo[c], hi[c]);
     const int T = p.horizon_steps;
@@ -626,8 +629,8 @@ struct Controller {
     const System<R> sys = system();
     for (int i = 0; i < iterations; ++i) {
       Batch<R> batch = sample(iteration);
-      const std::vector<R> costs = rollout_batch(sys, x0, batch, n_threads);
-      const Weights<R> w = it_weights(costs, static_cast<R>(p.lambda));
+      const std::vector<double> costs = rollout_batch(sys, x0, batch, n_threads);
+      const Weights<double> w = it_weights<double>(costs, p.lambda);
       plan = update_plan(batch, w.w);
       ++iteration;
     }
@@ -942,7 +945,7 @@ int oracle_rollout_costs(AnyController* h, const double* x0, const double* eps_i
     std::vector<R> x(sys.state_dim);
     for (int i = 0; i < sys.state_dim; ++i) x[i] = static_cast<R>(x0[i]);
     const auto costs = c.rollout_batch(sys, x.data(), b, n_threads);
-    for (size_t k = 0; k < costs.size(); ++k) costs_out[k] = static_cast<double>(costs[k]);
+    for (size_t k = 0; k < costs.size(); ++k) costs_out[k] = costs[k];
     if (eps_stored_out)
       for (size_t i = 0; i < b.eps.size(); ++i) eps_stored_out[i] = static_cast<double>(b.eps[i]);
     c.last_batch = std::move(b);
@@ -951,19 +954,17 @@ int oracle_rollout_costs(AnyController* h, const double* x0, const double* eps_i
 int oracle_weights(AnyController* h, const double* costs, double* w_out, double* rho,
                    double* eta) {
   return orc::dispatch(h, [&](auto& c) {
-    using R = typename std::decay_t<decltype(c.plan)>::value_type;
-    std::vector<R> s(costs, costs + c.p.samples);
-    const auto r = orc::it_weights<R>(s, static_cast<R>(c.p.lambda));
-    for (size_t k = 0; k < r.w.size(); ++k) w_out[k] = static_cast<double>(r.w[k]);
-    *rho = static_cast<double>(r.rho);
-    *eta = static_cast<double>(r.normalizer);
+    std::vector<double> s(costs, costs + c.p.samples);
+    const auto r = orc::it_weights<double>(s, c.p.lambda);
+    for (size_t k = 0; k < r.w.size(); ++k) w_out[k] = r.w[k];
+    *rho = r.rho;
+    *eta = r.normalizer;
   });
 }
 int oracle_update_plan(AnyController* h, const double* weights) {
   return orc::dispatch(h, [&](auto& c) {
-    using R = typename std::decay_t<decltype(c.plan)>::value_type;
     if (c.last_batch.K == 0) throw std::invalid_argument("update_plan: no rollout batch");
-    std::vector<R> w(weights, weights + c.p.samples);
+    std::vector<double> w(weights, weights + c.p.samples);
     c.plan = c.update_plan(c.last_batch, w);
   });
 }

@@ -28,13 +28,13 @@ template <class R>
 struct EpilogueArgs {
   int T, n_chunks, partial_stride;
   long long partials_ctrl_stride;
-  R lambda;
+  double lambda;
   R lo0, lo1, hi0, hi1;
   int sg_window;
-  R sg[kMaxSgWindow];
+  double sg[kMaxSgWindow];
   int slide, increment, plant;
-  const R* partials;     // [C][chunks][stride] (merge mode) or nullptr
-  const R* agg_in;       // [T][2] (caller-weights mode, controller 0) or nullptr
+  const Acc* partials;   // [C][chunks][stride] (merge mode) or nullptr
+  const Acc* agg_in;     // [T][2] (caller-weights mode, controller 0) or nullptr
   R* plan;               // [C][T][2]
   R* x0;                 // [C][8] (plant mode: advanced in place)
   uint64_t* iters;       // [C]
@@ -56,18 +56,18 @@ __device__ __forceinline__ int reflect_index(int i, int n) {
   return i;
 }
 
-// Dynamic smem: agg (2T) + U' (2T) + chunk scale factors (n_chunks) + MLP
-// scratch (2H).
+// Dynamic smem: agg (2T, double) + chunk scale factors (n_chunks, double) +
+// U' (2T, R) + MLP scratch (2H, R).
 template <class R, int H, class Sys, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__ EpilogueArgs<R> a,
                                                          const __grid_constant__ WeightHolder<R, H> wh) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
-  R* s_agg = reinterpret_cast<R*>(smem_raw);
-  R* s_new = s_agg + 2 * T;
-  R* s_scale = s_new + 2 * T;
-  R* s_mlp = s_scale + (a.partials ? a.n_chunks : 0);
-  __shared__ R s_red[BLOCK / 32];
+  Acc* s_agg = reinterpret_cast<Acc*>(smem_raw);
+  Acc* s_scale = s_agg + 2 * T;
+  R* s_new = reinterpret_cast<R*>(s_scale + (a.partials ? a.n_chunks : 0));
+  R* s_mlp = s_new + 2 * T;
+  __shared__ Acc s_red[BLOCK / 32];
   __shared__ int s_bad;
   __shared__ R s_u[2];
   const int ctrl = blockIdx.x;
@@ -76,33 +76,33 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
   R* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
 
   if (a.partials) {
-    const R* P = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride;
+    const Acc* P = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride;
     // any non-finite sample cost -> it_weights throws (weights.cpp:12)
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
-    R m = R(INFINITY);
+    Acc m = INFINITY;
     for (int c = threadIdx.x; c < a.n_chunks; c += BLOCK) {
-      const R* pc = P + static_cast<size_t>(c) * a.partial_stride;
-      if (pc[2] != R(0)) s_bad = 1;
+      const Acc* pc = P + static_cast<size_t>(c) * a.partial_stride;
+      if (pc[2] != 0.0) s_bad = 1;
       m = (pc[0] < m) ? pc[0] : m;
     }
-    const R rho = block_min<R, BLOCK>(m, s_red);
+    const Acc rho = block_min<Acc, BLOCK>(m, s_red);
     if (s_bad) {
       if (threadIdx.x == 0) st->code = 2;  // MPPI_ERR_NONFINITE
       return;
     }
-    R e = R(0);
+    Acc e = 0.0;
     for (int c = threadIdx.x; c < a.n_chunks; c += BLOCK) {
-      const R* pc = P + static_cast<size_t>(c) * a.partial_stride;
-      const R s = exp_r(div_r(-sub_rn(pc[0], rho), a.lambda));
+      const Acc* pc = P + static_cast<size_t>(c) * a.partial_stride;
+      const Acc s = exp(-(pc[0] - rho) / a.lambda);
       s_scale[c] = s;
       e = e + s * pc[1];
     }
-    const R eta = block_sum<R, BLOCK>(e, s_red);  // includes the barrier for s_scale
+    const Acc eta = block_sum<Acc, BLOCK>(e, s_red);  // includes the barrier for s_scale
     for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
-      R num = R(0);
+      Acc num = 0.0;
       for (int c = 0; c < a.n_chunks; ++c)
-        num = fma_r(s_scale[c], P[static_cast<size_t>(c) * a.partial_stride + kPartialHeader + i], num);
+        num = fma(s_scale[c], P[static_cast<size_t>(c) * a.partial_stride + kPartialHeader + i], num);
       s_agg[i] = num / eta;
     }
   } else {
@@ -116,16 +116,17 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
   const int half = a.sg_window / 2;
   for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
     const int t = i >> 1, c = i & 1;
-    R v;
+    Acc v;
     if (a.sg_window > 0) {
-      R acc = R(0);
+      Acc acc = 0.0;
       for (int j = -half; j <= half; ++j)
-        acc = add_rn(acc, mul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c]));
+        acc = __dadd_rn(acc, __dmul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c]));
       v = acc;
     } else {
       v = s_agg[i];
     }
-    const R nv = add_rn(plan[i], v);
+    // U' = U + SG(agg) in double, rounded once to R
+    const R nv = static_cast<R>(__dadd_rn(static_cast<Acc>(plan[i]), v));
     if (!isfinite_r(nv)) s_bad = 1;
     s_new[i] = nv;
   }
@@ -231,7 +232,8 @@ __global__ void slide_kernel(R* plan, int T, uint64_t* iters, StepStatus* status
   }
 }
 
-// it_weights (weights.cpp:8-25) on caller costs (parity entry point).
+// it_weights (weights.cpp:8-25) on caller costs (parity entry point); the
+// softmin runs in double for every precision (see Acc in rollout.cuh).
 template <class R, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) weights_kernel(const R* __restrict__ S, int K, R lambda,
                                                         R* w, R* rho_eta, int* bad_out) {

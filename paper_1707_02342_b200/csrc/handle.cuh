@@ -11,6 +11,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -18,6 +19,7 @@
 #include <vector>
 
 #include "epilogue.cuh"
+#include "ws_launch.hpp"
 #include "errors.hpp"
 #include "handle_iface.hpp"
 #include "host_util.hpp"
@@ -93,15 +95,25 @@ struct Handle final : HandleBase {
   }
   std::string variant_name() const override {
     char buf[160];
-    std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
-                  std::is_same<R, double>::value ? "f64" : "f32", H,
-                  cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic" : "vehicle_mlp", cfg.noise_mode, kBlock);
+    if (use_ws)
+      std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d> (chunk 32, %d chunks%s)", H, ws_L,
+                    cfg.noise_mode, n_chunks, merge_G ? ", pre-merged" : "");
+    else
+      std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
+                    std::is_same<R, double>::value ? "f64" : "f32", H,
+                    cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic" : "vehicle_mlp", cfg.noise_mode, kBlock);
     return buf;
   }
 
   mppi_gpu_config cfg{};
   int K = 0, T = 0, C = 1, H = 32, device = 0;
   int n_chunks = 0, chunks_per_rank = 0, chunk_lo = 0, chunk_hi = 0;
+  // K1 variant: warp-specialised fp32 kernel (chunk = 32 samples, L warps per
+  // chunk) for the vehicle model, generic one-sample-per-thread kernel
+  // (chunk = kBlock) otherwise.
+  bool use_ws = false;
+  int ws_L = 1, chunk_samples = kBlock;
+  int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   int rank = 0, world = 1;
   int zero_start = 0;
   int partial_stride = 0;
@@ -119,7 +131,8 @@ struct Handle final : HandleBase {
   bool has_mlp = false, has_map = false, has_noise = false;
 
   // device state
-  DevBuf<R> d_plan, d_x0, d_costs, d_partials, d_inj, d_decay, d_agg, d_w, d_rho_eta;
+  DevBuf<R> d_plan, d_x0, d_inj, d_decay;
+  DevBuf<Acc> d_costs, d_partials, d_partials2, d_agg, d_w, d_rho_eta;
   DevBuf<R> d_states, d_utrace, d_xtrace;
   DevBuf<double> d_eps_ref;
   DevBuf<uint64_t> d_iters, d_seeds, d_trace_base;
@@ -168,7 +181,8 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaEventCreate(&ev_b));
     CUDA_TRY(cudaEventCreate(&ev_it0));
     CUDA_TRY(cudaEventCreate(&ev_it1));
-    n_chunks = (K + kBlock - 1) / kBlock;
+    choose_variant();
+    n_chunks = (K + chunk_samples - 1) / chunk_samples;
     chunks_per_rank = n_chunks;
     chunk_lo = 0;
     chunk_hi = n_chunks;
@@ -183,6 +197,7 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaMemset(d_x0.p, 0, d_x0.n * sizeof(R)));
     d_costs.alloc(static_cast<size_t>(C) * K);
     d_partials.alloc(static_cast<size_t>(C) * partials_ctrl_stride);
+    setup_merge();
     d_agg.alloc(static_cast<size_t>(2) * T);
     d_iters.alloc(C);
     CUDA_TRY(cudaMemset(d_iters.p, 0, C * sizeof(uint64_t)));
@@ -224,6 +239,36 @@ struct Handle final : HandleBase {
     if (ev_it0) cudaEventDestroy(ev_it0);
     if (ev_it1) cudaEventDestroy(ev_it1);
     if (stream) cudaStreamDestroy(stream);
+  }
+
+  void choose_variant() {
+    const char* kv = std::getenv("MPPI_KERNEL");
+    const bool force_generic = kv && std::string(kv) == "generic";
+    use_ws = std::is_same<R, float>::value && cfg.system == MPPI_SYSTEM_VEHICLE_MLP && !force_generic;
+    if (!use_ws) {
+      chunk_samples = kBlock;
+      return;
+    }
+    chunk_samples = 32;
+    // enough warps to cover the 148 x 4 sub-partitions several times over:
+    // L = clamp(pow2floor(2048 * 32 / K), 1, 8)
+    int L = 1;
+    while (L < 8 && static_cast<long long>(2 * L) * K <= 2048LL * 32) L *= 2;
+    if (const char* lv = std::getenv("MPPI_WS_L")) {
+      const int want = std::atoi(lv);
+      if (want == 1 || want == 2 || want == 4 || want == 8) L = want;
+    }
+    if (H == 64 && L < 2) L = 2;  // the H = 64 kernels split the hidden layer over >= 2 warps
+    ws_L = L;
+  }
+  void setup_merge() {
+    merge_G = 0;
+    n_merged = n_chunks;
+    if (n_chunks > 256) {
+      merge_G = 32;
+      n_merged = (n_chunks + merge_G - 1) / merge_G;
+      d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
+    }
   }
 
   static void validate_config(const mppi_gpu_config& c) {
@@ -437,6 +482,7 @@ struct Handle final : HandleBase {
     a.gamma = static_cast<R>(cfg.gamma);
     a.sigma0 = static_cast<R>(cfg.sigma_diag[0]);
     a.sigma1 = static_cast<R>(cfg.sigma_diag[1]);
+    a.dlambda = cfg.lambda;
     a.dscale0 = std::sqrt(cfg.sigma_diag[0]);
     a.dscale1 = std::sqrt(cfg.sigma_diag[1]);
     a.scale0 = static_cast<R>(a.dscale0);
@@ -518,7 +564,15 @@ struct Handle final : HandleBase {
     using type = T_;
   };
 
-  size_t rollout_smem() const { return sizeof(R) * (2 * T + (kBlock / 32) * 2 * T); }
+  size_t rollout_smem() const { return sizeof(Acc) * (kBlock / 32) * 2 * T + sizeof(R) * 2 * T; }
+
+  void launch_ws(const RolloutArgs<R>& a, int mode, dim3 grid) {
+    if constexpr (std::is_same<R, float>::value) {
+      const size_t smem = sizeof(float) * 2 * T;
+      if (H == 32) CUDA_TRY(launch_rollout_ws_h32(a, holder<32>(), mode, ws_L, grid, smem, stream));
+      else CUDA_TRY(launch_rollout_ws_h64(a, holder<64>(), mode, ws_L, grid, smem, stream));
+    }
+  }
 
   // events: bracket the launch with ev_a/ev_b without synchronising (used
   // inside captured graphs; the caller reads the elapsed time afterwards).
@@ -526,16 +580,23 @@ struct Handle final : HandleBase {
     const RolloutArgs<R> a = rollout_args();
     const size_t smem = rollout_smem();
     const dim3 grid(chunk_hi - chunk_lo, C);
-    if (profile || events) CUDA_TRY(cudaEventRecord(ev_a, stream));
-    dispatch(mode, [&]<int HH, class Sys, int Mode>() {
-      auto kern = rollout_kernel<R, HH, Sys, Mode, kBlock>;
-      if (smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      kern<<<grid, kBlock, smem, stream>>>(a, holder<HH>());
-    });
+    // inside stream capture an event record is only a dependency edge unless
+    // it is marked external; external records become graph event nodes
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_a, stream, cudaEventRecordExternal));
+    else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
+    if (use_ws) {
+      launch_ws(a, mode, grid);
+    } else {
+      dispatch(mode, [&]<int HH, class Sys, int Mode>() {
+        auto kern = rollout_kernel<R, HH, Sys, Mode, kBlock>;
+        if (smem > 48 * 1024)
+          CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<grid, kBlock, smem, stream>>>(a, holder<HH>());
+      });
+    }
     ++launches;
     CUDA_TRY(cudaGetLastError());
-    if (events) CUDA_TRY(cudaEventRecord(ev_b, stream));
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_b, stream, cudaEventRecordExternal));
     if (profile && !events) {
       CUDA_TRY(cudaEventRecord(ev_b, stream));
       CUDA_TRY(cudaEventSynchronize(ev_b));
@@ -546,31 +607,40 @@ struct Handle final : HandleBase {
     }
   }
 
+  void enqueue_premerge() {
+    if (!merge_G) return;
+    const dim3 grid(n_merged, C);
+    merge_chunks_kernel<><<<grid, 256, 0, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
+                                                   merge_G, cfg.lambda, d_partials2.p,
+                                                   static_cast<long long>(n_merged) * partial_stride);
+    ++launches;
+    CUDA_TRY(cudaGetLastError());
+  }
+
   void enqueue_exchange() {
     if (world <= 1) return;
     const size_t count = static_cast<size_t>(chunks_per_rank) * partial_stride;
-    R* base = d_partials.p;
-    const ncclDataType_t dt = std::is_same<R, double>::value ? ncclFloat64 : ncclFloat32;
-    NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, dt, comm, stream));
+    Acc* base = d_partials.p;
+    NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, ncclFloat64, comm, stream));
   }
 
   EpilogueArgs<R> epilogue_args(bool merge, bool slide, bool increment, bool plant, bool trace) const {
     EpilogueArgs<R> e{};
     e.T = T;
-    e.n_chunks = n_chunks;
+    e.n_chunks = merge_G ? n_merged : n_chunks;
     e.partial_stride = partial_stride;
-    e.partials_ctrl_stride = partials_ctrl_stride;
-    e.lambda = static_cast<R>(cfg.lambda);
+    e.partials_ctrl_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
+    e.lambda = cfg.lambda;
     e.lo0 = static_cast<R>(cfg.bounds_lower[0]);
     e.lo1 = static_cast<R>(cfg.bounds_lower[1]);
     e.hi0 = static_cast<R>(cfg.bounds_upper[0]);
     e.hi1 = static_cast<R>(cfg.bounds_upper[1]);
     e.sg_window = static_cast<int>(sg.size());
-    for (size_t i = 0; i < sg.size(); ++i) e.sg[i] = static_cast<R>(sg[i]);
+    for (size_t i = 0; i < sg.size(); ++i) e.sg[i] = sg[i];
     e.slide = slide;
     e.increment = increment;
     e.plant = plant;
-    e.partials = merge ? d_partials.p : nullptr;
+    e.partials = merge ? (merge_G ? d_partials2.p : d_partials.p) : nullptr;
     e.agg_in = merge ? nullptr : d_agg.p;
     e.plan = d_plan.p;
     e.x0 = d_x0.p;
@@ -585,7 +655,7 @@ struct Handle final : HandleBase {
   }
   void enqueue_epilogue(bool merge, bool slide, bool increment, bool plant, bool trace, int ctrls) {
     const EpilogueArgs<R> e = epilogue_args(merge, slide, increment, plant, trace);
-    const size_t smem = sizeof(R) * (4 * T + (merge ? n_chunks : 0) + 2 * 64);
+    const size_t smem = sizeof(Acc) * (2 * T + (merge ? (merge_G ? n_merged : n_chunks) : 0)) + sizeof(R) * (2 * T + 2 * 64);
     dispatch(kPhilox, [&]<int HH, class Sys, int Mode>() {
       auto kern = epilogue_kernel<R, HH, Sys, kEpiBlock>;
       if (smem > 48 * 1024)
@@ -624,6 +694,7 @@ struct Handle final : HandleBase {
         profile = false;
         enqueue_rollout(cfg.noise_mode, /*events=*/which == 2);
         enqueue_exchange();
+        enqueue_premerge();
         enqueue_epilogue(true, slide, /*increment=*/slide, plant, trace, C);
         profile = prof;
         if (which != 2)
@@ -701,6 +772,7 @@ struct Handle final : HandleBase {
     for (int i = 0; i < iterations; ++i) {
       enqueue_rollout(cfg.noise_mode);
       enqueue_exchange();
+      enqueue_premerge();
       enqueue_epilogue(true, false, true, false, false, C);
     }
     CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
@@ -819,10 +891,8 @@ struct Handle final : HandleBase {
     const int mode = effective_mode(eps_in != nullptr);
     enqueue_rollout(mode);
     enqueue_exchange();
-    std::vector<R> c(static_cast<size_t>(K));
-    CUDA_TRY(cudaMemcpyAsync(c.data(), d_costs.p, K * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(costs_out, d_costs.p, K * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
-    for (int k = 0; k < K; ++k) costs_out[k] = static_cast<double>(c[k]);
     batch_valid = true;
     batch_injected = eps_in != nullptr || cfg.noise_mode == MPPI_NOISE_INJECTED;
     CUDA_TRY(cudaMemcpy(&batch_iteration, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
@@ -844,34 +914,31 @@ struct Handle final : HandleBase {
     }
   }
 
+  // it_weights on caller costs; the softmin runs in double for every
+  // precision (Acc, rollout.cuh), as in the fused path.
   void weights(const double* costs, double* w_out, double* rho, double* eta) {
-    std::vector<R> c(K);
-    for (int k = 0; k < K; ++k) c[k] = static_cast<R>(costs[k]);
-    DevBuf<R> d_c;
+    DevBuf<Acc> d_c;
     d_c.alloc(K);
     d_w.alloc(K);
-    CUDA_TRY(cudaMemcpyAsync(d_c.p, c.data(), K * sizeof(R), cudaMemcpyHostToDevice, stream));
-    weights_kernel<R, 1024><<<1, 1024, 0, stream>>>(d_c.p, K, static_cast<R>(cfg.lambda), d_w.p, d_rho_eta.p, d_bad.p);
+    CUDA_TRY(cudaMemcpyAsync(d_c.p, costs, K * sizeof(Acc), cudaMemcpyHostToDevice, stream));
+    weights_kernel<Acc, 1024><<<1, 1024, 0, stream>>>(d_c.p, K, cfg.lambda, d_w.p, d_rho_eta.p, d_bad.p);
     ++launches;
     CUDA_TRY(cudaGetLastError());
     int bad = 0;
-    R re[2];
+    Acc re[2];
     CUDA_TRY(cudaMemcpyAsync(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaMemcpyAsync(re, d_rho_eta.p, 2 * sizeof(R), cudaMemcpyDeviceToHost, stream));
-    CUDA_TRY(cudaMemcpyAsync(c.data(), d_w.p, K * sizeof(R), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(re, d_rho_eta.p, 2 * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(w_out, d_w.p, K * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     if (bad) throw Error(MPPI_ERR_NONFINITE, "it_weights: non-finite cost");
-    for (int k = 0; k < K; ++k) w_out[k] = static_cast<double>(c[k]);
-    *rho = static_cast<double>(re[0]);
-    *eta = static_cast<double>(re[1]);
+    *rho = re[0];
+    *eta = re[1];
   }
 
   void update_plan(const double* w) {
     if (!batch_valid) throw_invalid("update_plan: no rollout batch");
-    std::vector<R> wr(K);
-    for (int k = 0; k < K; ++k) wr[k] = static_cast<R>(w[k]);
     d_w.alloc(K);
-    CUDA_TRY(cudaMemcpyAsync(d_w.p, wr.data(), K * sizeof(R), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_w.p, w, K * sizeof(Acc), cudaMemcpyHostToDevice, stream));
     uint64_t saved = 0;
     CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(d_iters.p, &batch_iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
@@ -905,10 +972,19 @@ struct Handle final : HandleBase {
     uint64_t saved = 0;
     CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(d_iters.p, &batch_iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
-    const RolloutArgs<R> a = rollout_args();
-    dispatch(effective_mode(batch_injected), [&]<int HH, class Sys, int Mode>() {
-      rollout_states_kernel<R, HH, Sys, Mode><<<1, 32, 0, stream>>>(a, holder<HH>(), sample, d_states.p);
-    });
+    RolloutArgs<R> a = rollout_args();
+    if (use_ws) {
+      // trace the production kernel itself: sample `sample`'s state per step
+      a.trace_states = d_states.p;
+      a.trace_k = sample;
+      a.chunk0 = 0;
+      CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
+      launch_ws(a, effective_mode(batch_injected), dim3(n_chunks, 1));
+    } else {
+      dispatch(effective_mode(batch_injected), [&]<int HH, class Sys, int Mode>() {
+        rollout_states_kernel<R, HH, Sys, Mode><<<1, 32, 0, stream>>>(a, holder<HH>(), sample, d_states.p);
+      });
+    }
     ++launches;
     CUDA_TRY(cudaGetLastError());
     std::vector<R> s(d_states.n);
@@ -931,8 +1007,10 @@ struct Handle final : HandleBase {
     chunks_per_rank = (n_chunks + w - 1) / w;
     chunk_lo = std::min(n_chunks, r * chunks_per_rank);
     chunk_hi = std::min(n_chunks, (r + 1) * chunks_per_rank);
-    if (chunk_hi <= chunk_lo) throw_invalid("set_comm: more ranks than sample chunks (128 samples each)");
-    d_partials.alloc(static_cast<size_t>(w) * chunks_per_rank * partial_stride);
+    if (chunk_hi <= chunk_lo) throw_invalid("set_comm: more ranks than sample chunks");
+    partials_ctrl_stride = static_cast<long long>(w) * chunks_per_rank * partial_stride;
+    d_partials.alloc(static_cast<size_t>(partials_ctrl_stride));
+    setup_merge();
     if (w > 1) {
       ncclUniqueId uid;
       static_assert(sizeof(uid) == 128, "ncclUniqueId must be 128 bytes");

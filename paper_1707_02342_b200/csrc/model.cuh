@@ -17,7 +17,7 @@ namespace mppi_dev {
 // Device layout of MlpWeights (dynamics.hpp:110-119), transposed to
 // input-major so that one input feeds consecutive outputs (pairwise FFMA2).
 template <class R, int H>
-struct MlpParams {
+struct alignas(16) MlpParams {
   R w1t[6][H];   // w1t[i][j] = W1[j][i]
   R b1[H];
   R w2t[H][H];   // w2t[i][j] = W2[j][i]

@@ -21,6 +21,14 @@ namespace mppi_dev {
 
 constexpr int kPartialHeader = 4;  // rho, eta, bad, reserved
 
+// Mixed precision: the per-step dynamics and cost terms run in R (fp32 in
+// production); the T-term cost sum, the softmin (rho, eta, w) and the
+// weighted-noise numerators are accumulated in double.  With costs ~1e5 an
+// fp32 running sum carries ~0.1 absolute error, which lambda = 6.66 turns into
+// ~1% weight error; the double accumulators cost O(K T) adds against the
+// O(K T H^2) FMAs of the MLP.
+using Acc = double;
+
 template <class R>
 struct RolloutArgs {
   int K, T;
@@ -29,7 +37,7 @@ struct RolloutArgs {
   int partial_stride;     // kPartialHeader + 2T
   long long partials_ctrl_stride;
   R lambda, gamma, sigma0, sigma1, scale0, scale1;
-  double dscale0, dscale1;
+  double dscale0, dscale1, dlambda;
   SystemArgs<R> sys;
   const R* plan;          // [C][T][2]
   const R* x0;            // [C][8]
@@ -40,8 +48,10 @@ struct RolloutArgs {
   const uint64_t* seeds;  // [C]
   const uint64_t* iters;  // [C]
   const int* abort_flag;  // [C] sticky status codes: nonzero -> skip
-  R* costs;               // [C][K]
-  R* partials;            // [C][chunks][partial_stride]
+  Acc* costs;             // [C][K]
+  Acc* partials;          // [C][chunks][partial_stride]
+  R* trace_states;        // (T+1) x 7 trajectory of sample trace_k (or nullptr)
+  int trace_k;
 };
 
 template <class R, int Mode>
@@ -67,7 +77,7 @@ __device__ __forceinline__ NoiseStream<R, Mode> make_noise(const RolloutArgs<R>&
 // Rollout of one sample (the body of the rollout_batch k-loop).  If
 // `states_out` is non-null, the (T+1) x state_dim trajectory is written.
 template <class R, int H, class Sys, int Mode>
-__device__ __forceinline__ R rollout_one(const RolloutArgs<R>& a, const MlpParams<R, H>& w,
+__device__ __forceinline__ Acc rollout_one(const RolloutArgs<R>& a, const MlpParams<R, H>& w,
                                          const R* __restrict__ plan, int ctrl, int k,
                                          R* states_out) {
   NoiseStream<R, Mode> ns = make_noise<R, Mode>(a, ctrl, k);
@@ -89,7 +99,7 @@ __device__ __forceinline__ R rollout_one(const RolloutArgs<R>& a, const MlpParam
   }
   const R half_lambda = mul_rn(R(0.5), a.lambda);
   const R gml = sub_rn(a.gamma, a.lambda);
-  R cost = R(0);
+  Acc cost = 0.0;
   // The running cost of step t needs the costmap at x_{t+1}; its four taps are
   // fetched right after the step and consumed one MLP later, hiding the L2
   // latency behind the next step's FMAs.
@@ -121,7 +131,7 @@ __device__ __forceinline__ R rollout_one(const RolloutArgs<R>& a, const MlpParam
       if (t > 0) {
         const R h = map_interp(q);
         const R rc = state_cost_h(h, p_roll, p_vx, p_vy, a.sys.decay_pow[t - 1], a.sys.cost);
-        cost = add_rn(cost, add_rn(rc, p_coup));
+        cost += static_cast<Acc>(add_rn(rc, p_coup));
       }
       q = map_fetch(map, x[0], x[1]);
       p_roll = x[3];
@@ -129,16 +139,16 @@ __device__ __forceinline__ R rollout_one(const RolloutArgs<R>& a, const MlpParam
       p_vy = x[5];
       p_coup = coupling;
     } else {
-      cost = add_rn(cost, add_rn(Sys::cost(x, a.sys), coupling));
+      cost += static_cast<Acc>(add_rn(Sys::cost(x, a.sys), coupling));
     }
   }
   if constexpr (Sys::kHasMap) {
     const R h = map_interp(q);
     const R rc = state_cost_h(h, p_roll, p_vx, p_vy, a.sys.decay_pow[a.T - 1], a.sys.cost);
-    cost = add_rn(cost, add_rn(rc, p_coup));
+    cost += static_cast<Acc>(add_rn(rc, p_coup));
     // terminal cost = state_cost(x_T, T) (controller.cpp:27-30): same taps.
     if (a.sys.with_terminal)
-      cost = add_rn(cost, state_cost_h(h, p_roll, p_vx, p_vy, a.sys.decay_pow[a.T], a.sys.cost));
+      cost += static_cast<Acc>(state_cost_h(h, p_roll, p_vx, p_vy, a.sys.decay_pow[a.T], a.sys.cost));
   }
   return cost;
 }
@@ -170,14 +180,14 @@ __device__ __forceinline__ R block_sum(R v, R* s_red) {
 }
 
 // K1.  grid = (chunks of this rank, controllers), block = BLOCK samples.
-// Dynamic smem: plan (2T) + per-warp numerators (BLOCK/32 x 2T).
+// Dynamic smem: per-warp numerators (BLOCK/32 x 2T, double) + plan (2T, R).
 template <class R, int H, class Sys, int Mode, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ RolloutArgs<R> a,
                                                         const __grid_constant__ WeightHolder<R, H> wh) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* s_plan = reinterpret_cast<R*>(smem_raw);
-  R* s_num = s_plan + 2 * a.T;
-  __shared__ R s_red[BLOCK / 32];
+  Acc* s_num = reinterpret_cast<Acc*>(smem_raw);
+  R* s_plan = reinterpret_cast<R*>(s_num + (BLOCK / 32) * 2 * a.T);
+  __shared__ Acc s_red[BLOCK / 32];
   const int ctrl = blockIdx.y;
   if (a.abort_flag[ctrl] != 0) return;
   const int chunk = a.chunk0 + blockIdx.x;
@@ -187,17 +197,17 @@ __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ 
   for (int i = threadIdx.x; i < 2 * T; i += BLOCK) s_plan[i] = a.plan[static_cast<size_t>(ctrl) * 2 * T + i];
   __syncthreads();
 
-  R cost = R(0);
+  Acc cost = 0.0;
   if (valid) {
     cost = rollout_one<R, H, Sys, Mode>(a, wh.get(), s_plan, ctrl, k, nullptr);
     a.costs[static_cast<size_t>(ctrl) * a.K + k] = cost;
   }
-  const bool bad = valid && !isfinite_r(cost);
+  const bool bad = valid && !isfinite(cost);
   const int any_bad = __syncthreads_or(bad);
-  const R rho = block_min<R, BLOCK>(valid ? cost : R(INFINITY), s_red);
+  const Acc rho = block_min<Acc, BLOCK>(valid ? cost : Acc(INFINITY), s_red);
   // it_weights (weights.cpp:15-23) relative to the chunk minimum.
-  const R wk = valid ? exp_r(div_r(-sub_rn(cost, rho), a.lambda)) : R(0);
-  const R eta = block_sum<R, BLOCK>(wk, s_red);
+  const Acc wk = valid ? exp(-(cost - rho) / a.dlambda) : 0.0;
+  const Acc eta = block_sum<Acc, BLOCK>(wk, s_red);
 
   // Weighted numerator over the regenerated batch.
   NoiseStream<R, Mode> ns = make_noise<R, Mode>(a, ctrl, valid ? k : 0);
@@ -212,18 +222,18 @@ __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ 
         e1 = sub_rn(e1, s_plan[2 * t + 1]);
       }
     }
-    const R n0 = warp_sum(wk * e0);
-    const R n1 = warp_sum(wk * e1);
+    const Acc n0 = warp_sum(wk * static_cast<Acc>(e0));
+    const Acc n1 = warp_sum(wk * static_cast<Acc>(e1));
     if (lane == 0) {
       s_num[(wid * T + t) * 2] = n0;
       s_num[(wid * T + t) * 2 + 1] = n1;
     }
   }
   __syncthreads();
-  R* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
-           static_cast<size_t>(chunk) * a.partial_stride;
+  Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
+             static_cast<size_t>(chunk) * a.partial_stride;
   for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
-    R s = s_num[i];
+    Acc s = s_num[i];
 #pragma unroll
     for (int w2 = 1; w2 < BLOCK / 32; ++w2) s = s + s_num[w2 * 2 * T + i];
     out[kPartialHeader + i] = s;
@@ -231,8 +241,8 @@ __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ 
   if (threadIdx.x == 0) {
     out[0] = rho;
     out[1] = eta;
-    out[2] = any_bad ? R(1) : R(0);
-    out[3] = R(0);
+    out[2] = any_bad ? 1.0 : 0.0;
+    out[3] = 0.0;
   }
 }
 
@@ -272,22 +282,23 @@ __global__ void materialize_batch_kernel(const __grid_constant__ RolloutArgs<R> 
 // One thread per timestep; eps' regenerated per (k, t).
 template <class R, int Mode>
 __global__ void weighted_agg_kernel(const __grid_constant__ RolloutArgs<R> a,
-                                    const R* __restrict__ w, R* agg) {
+                                    const Acc* __restrict__ w, Acc* agg) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.T) return;
   const uint64_t it = a.iters[0], seed = a.seeds[0];
-  R s0 = R(0), s1 = R(0);
+  Acc s0 = 0.0, s1 = 0.0;
   const R u0 = a.plan[2 * t], u1 = a.plan[2 * t + 1];
+  const uint64_t prefix = ref_hash_prefix(seed, it);
   for (int k = 0; k < a.K; ++k) {
-    const R wk = w[k];
-    if (wk == R(0)) continue;
+    const Acc wk = w[k];
+    if (wk == 0.0) continue;
     R e0, e1;
     if constexpr (Mode == kInjected) {
       e0 = a.inj[(static_cast<size_t>(t) * a.K + k) * 2];
       e1 = a.inj[(static_cast<size_t>(t) * a.K + k) * 2 + 1];
     } else if constexpr (Mode == kRefSplitmix) {
       double z0, z1;
-      ref_normal_pair(ref_hash_prefix(seed, it), static_cast<uint64_t>(k), static_cast<uint64_t>(t), z0, z1);
+      ref_normal_pair(prefix, static_cast<uint64_t>(k), static_cast<uint64_t>(t), z0, z1);
       e0 = static_cast<R>(a.dscale0 * z0);
       e1 = static_cast<R>(a.dscale1 * z1);
     } else {
@@ -302,8 +313,8 @@ __global__ void weighted_agg_kernel(const __grid_constant__ RolloutArgs<R> a,
       e0 = sub_rn(e0, u0);
       e1 = sub_rn(e1, u1);
     }
-    s0 = add_rn(s0, mul_rn(wk, e0));
-    s1 = add_rn(s1, mul_rn(wk, e1));
+    s0 = __dadd_rn(s0, __dmul_rn(wk, static_cast<Acc>(e0)));
+    s1 = __dadd_rn(s1, __dmul_rn(wk, static_cast<Acc>(e1)));
   }
   agg[2 * t] = s0;
   agg[2 * t + 1] = s1;
@@ -319,6 +330,39 @@ __global__ void inject_transpose_kernel(const double* __restrict__ ref, int K, i
     const int t = static_cast<int>(i / K);
     dev[i * 2] = static_cast<R>(ref[(static_cast<size_t>(k) * 2) * T + t]);
     dev[i * 2 + 1] = static_cast<R>(ref[(static_cast<size_t>(k) * 2 + 1) * T + t]);
+  }
+}
+
+// Pre-merge of G consecutive chunk partials into one (same format), in fixed
+// order, when a launch produced many small chunks.  grid = (ceil(n_in / G), C).
+template <int kUnused = 0>
+__global__ void merge_chunks_kernel(const Acc* __restrict__ in, int n_in, int stride, long long in_ctrl_stride,
+                                    int G, double lambda, Acc* __restrict__ out, long long out_ctrl_stride) {
+  const int b = blockIdx.x, ctrl = blockIdx.y;
+  const int c0 = b * G, c1 = min(n_in, c0 + G);
+  const Acc* P = in + static_cast<size_t>(ctrl) * in_ctrl_stride;
+  Acc rho = INFINITY, bad = 0.0;
+  for (int c = c0; c < c1; ++c) {
+    const Acc r = P[static_cast<size_t>(c) * stride];
+    rho = (r < rho) ? r : rho;
+    if (P[static_cast<size_t>(c) * stride + 2] != 0.0) bad = 1.0;
+  }
+  Acc* o = out + static_cast<size_t>(ctrl) * out_ctrl_stride + static_cast<size_t>(b) * stride;
+  for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+    if (i == 0) {
+      o[0] = rho;
+    } else if (i == 2) {
+      o[2] = bad;
+    } else if (i == 3) {
+      o[3] = 0.0;
+    } else {
+      Acc s = 0.0;
+      for (int c = c0; c < c1; ++c) {
+        const Acc* pc = P + static_cast<size_t>(c) * stride;
+        s = fma(exp(-(pc[0] - rho) / lambda), pc[i], s);
+      }
+      o[i] = s;
+    }
   }
 }
 

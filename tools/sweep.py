@@ -1,0 +1,55 @@
+#!/usr/bin/env python3
+"""Kernel-variant sweep: device ms per IT-MPPI iteration (closed loop, L2
+flushed between iterations) for each K1 variant, on the BASELINE configs."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def run(cfg, K, variant, L, steps=30):
+    os.environ.pop("MPPI_KERNEL", None)
+    os.environ.pop("MPPI_WS_L", None)
+    if variant == "generic":
+        os.environ["MPPI_KERNEL"] = "generic"
+    elif L:
+        os.environ["MPPI_WS_L"] = str(L)
+    from paper_1707_02342_b200 import workload
+    from paper_1707_02342_b200.api import Controller
+    w = workload.make(cfg, samples=K)
+    c = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox")
+    c.set_mlp(w.mlp)
+    c.set_costmap(w.costmap)
+    c.closed_loop_timed(w.x0[0], 5, 256 << 20)
+    c.profile_read(reset=True)
+    ms = c.closed_loop_timed(w.x0[0], steps, 256 << 20)
+    k1_ms, n = c.profile_read(reset=True)
+    k1 = k1_ms / max(n, 1)
+    T = w.params.horizon_steps
+    fl = K * T * workload.flops_per_sample_step(w.hidden)
+    out = {"cfg": cfg, "K": K, "T": T, "H": w.hidden, "variant": c.kernel_variant, "ms_per_iter": ms / steps,
+           "k1_ms": k1, "k1_tflops": fl / (k1 * 1e-3) / 1e12 if k1 > 0 else None,
+           "Gsteps_per_s": K * T / (ms / steps * 1e-3) / 1e9}
+    print(json.dumps(out), flush=True)
+    c.close()
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    cases = []
+    for cfg, K in (("c1", 16384), ("c0", 1920), ("c2", 65536), ("c4", 1024), ("c4", 262144), ("c4", 1048576)):
+        for variant, L in (("generic", 0), ("ws", 1), ("ws", 2), ("ws", 4), ("ws", 8)):
+            if cfg == "c2" and variant == "ws" and L == 1:
+                continue
+            if K >= 262144 and variant == "generic":
+                continue
+            cases.append((cfg, K, variant, L))
+    for cfg, K, variant, L in cases:
+        if which != "all" and cfg != which:
+            continue
+        try:
+            run(cfg, K, variant, L, steps=10 if K >= 262144 else 30)
+        except Exception as e:  # keep sweeping
+            print(json.dumps({"cfg": cfg, "K": K, "variant": variant, "L": L, "error": str(e)}), flush=True)
