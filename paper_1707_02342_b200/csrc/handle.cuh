@@ -96,8 +96,8 @@ struct Handle final : HandleBase {
   std::string variant_name() const override {
     char buf[160];
     if (use_ws)
-      std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d> (chunk 32, %d chunks%s)", H, ws_L,
-                    cfg.noise_mode, n_chunks, merge_G ? ", pre-merged" : "");
+      std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks%s)", H, ws_L,
+                    cfg.noise_mode, ws_smem_w ? "smem-weights" : "const-weights", n_chunks, merge_G ? ", pre-merged" : "");
     else
       std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
                     std::is_same<R, double>::value ? "f64" : "f32", H,
@@ -113,6 +113,7 @@ struct Handle final : HandleBase {
   // (chunk = kBlock) otherwise.
   bool use_ws = false;
   int ws_L = 1, chunk_samples = kBlock;
+  bool ws_smem_w = true;  // weights staged in shared memory (vs constant bank)
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   int rank = 0, world = 1;
   int zero_start = 0;
@@ -258,6 +259,7 @@ struct Handle final : HandleBase {
       const int want = std::atoi(lv);
       if (want == 1 || want == 2 || want == 4 || want == 8) L = want;
     }
+    if (const char* sv = std::getenv("MPPI_WS_SMEM_W")) ws_smem_w = std::atoi(sv) != 0;
     if (H == 64 && L < 2) L = 2;  // the H = 64 kernels split the hidden layer over >= 2 warps
     ws_L = L;
   }
@@ -569,8 +571,8 @@ struct Handle final : HandleBase {
   void launch_ws(const RolloutArgs<R>& a, int mode, dim3 grid) {
     if constexpr (std::is_same<R, float>::value) {
       const size_t smem = sizeof(float) * 2 * T;
-      if (H == 32) CUDA_TRY(launch_rollout_ws_h32(a, holder<32>(), mode, ws_L, grid, smem, stream));
-      else CUDA_TRY(launch_rollout_ws_h64(a, holder<64>(), mode, ws_L, grid, smem, stream));
+      if (H == 32) CUDA_TRY(launch_rollout_ws_h32(a, holder<32>(), mode, ws_L, ws_smem_w, grid, smem, stream));
+      else CUDA_TRY(launch_rollout_ws_h64(a, holder<64>(), mode, ws_L, ws_smem_w, grid, smem, stream));
     }
   }
 

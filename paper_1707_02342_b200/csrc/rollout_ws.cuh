@@ -64,7 +64,10 @@ struct WsSmem {
   Acc w[32];                   // softmin weights of the group
 };
 
-template <int H, int L, int Mode>
+// SW = true stages the weights in shared memory (LDS.128 into registers);
+// SW = false reads them from the kernel-parameter constant bank (LDCU into
+// uniform registers).
+template <int H, int L, int Mode, bool SW>
 __global__ void __launch_bounds__(32 * L) rollout_ws_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const __grid_constant__ WeightHolder<float, H> wh) {
   static_assert(H % (2 * L) == 0, "each role owns an even number of hidden units");
@@ -83,9 +86,18 @@ __global__ void __launch_bounds__(32 * L) rollout_ws_kernel(const __grid_constan
   const bool valid = k < a.K;
   const int T = a.T;
   for (int i = threadIdx.x; i < 2 * T; i += 32 * L) s_plan[i] = a.plan[static_cast<size_t>(ctrl) * 2 * T + i];
+  __shared__ __align__(16) MlpParams<float, SW ? H : 2> s_w;
+  if constexpr (SW) {
+    const float4* src = reinterpret_cast<const float4*>(&wh.get());
+    float4* dst = reinterpret_cast<float4*>(&s_w);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<float, H>) / 16); i += 32 * L) dst[i] = src[i];
+  }
   __syncthreads();
 
-  const MlpParams<float, H>& w = wh.get();
+  const MlpParams<float, H>& w = [&]() -> const MlpParams<float, H>& {
+    if constexpr (SW) return s_w;
+    else return wh.get();
+  }();
   const bool zm = k >= a.zero_start;
   const float dt = a.sys.dt;
 

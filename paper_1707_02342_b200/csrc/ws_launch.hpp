@@ -11,8 +11,8 @@
 namespace mppi_host {
 
 cudaError_t launch_rollout_ws_h32(const mppi_dev::RolloutArgs<float>& a, const mppi_dev::WeightHolder<float, 32>& w,
-                                  int mode, int L, dim3 grid, size_t smem, cudaStream_t stream);
+                                  int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
 cudaError_t launch_rollout_ws_h64(const mppi_dev::RolloutArgs<float>& a, const mppi_dev::WeightHolder<float, 64>& w,
-                                  int mode, int L, dim3 grid, size_t smem, cudaStream_t stream);
+                                  int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
 
 }  // namespace mppi_host

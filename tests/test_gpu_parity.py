@@ -315,4 +315,4 @@ def test_kernel_variant_and_launch_count():
     n0 = g.launch_count
     g.mpc_step(w.x0[0])
     assert g.launch_count - n0 == 2  # K1 rollout + K2 epilogue
-    assert "rollout_kernel" in g.kernel_variant
+    assert "rollout_ws_kernel" in g.kernel_variant  # the fp32 vehicle path is the warp-specialised K1

@@ -9,13 +9,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def run(cfg, K, variant, L, steps=30):
-    os.environ.pop("MPPI_KERNEL", None)
-    os.environ.pop("MPPI_WS_L", None)
+def run(cfg, K, variant, L, steps=30, sw=1):
+    for v in ("MPPI_KERNEL", "MPPI_WS_L", "MPPI_WS_SMEM_W"):
+        os.environ.pop(v, None)
     if variant == "generic":
         os.environ["MPPI_KERNEL"] = "generic"
     elif L:
         os.environ["MPPI_WS_L"] = str(L)
+    os.environ["MPPI_WS_SMEM_W"] = str(sw)
     from paper_1707_02342_b200 import workload
     from paper_1707_02342_b200.api import Controller
     w = workload.make(cfg, samples=K)
@@ -39,17 +40,18 @@ def run(cfg, K, variant, L, steps=30):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     cases = []
-    for cfg, K in (("c1", 16384), ("c0", 1920), ("c2", 65536), ("c4", 1024), ("c4", 262144), ("c4", 1048576)):
-        for variant, L in (("generic", 0), ("ws", 1), ("ws", 2), ("ws", 4), ("ws", 8)):
+    for cfg, K in (("c1", 16384), ("c0", 1920), ("c2", 65536), ("c4", 262144)):
+        for variant, L, sw in (("generic", 0, 0), ("ws", 1, 0), ("ws", 1, 1), ("ws", 2, 1), ("ws", 4, 1),
+                               ("ws", 8, 1), ("ws", 2, 0), ("ws", 4, 0)):
             if cfg == "c2" and variant == "ws" and L == 1:
                 continue
             if K >= 262144 and variant == "generic":
                 continue
-            cases.append((cfg, K, variant, L))
-    for cfg, K, variant, L in cases:
+            cases.append((cfg, K, variant, L, sw))
+    for cfg, K, variant, L, sw in cases:
         if which != "all" and cfg != which:
             continue
         try:
-            run(cfg, K, variant, L, steps=10 if K >= 262144 else 30)
+            run(cfg, K, variant, L, steps=10 if K >= 262144 else 30, sw=sw)
         except Exception as e:  # keep sweeping
             print(json.dumps({"cfg": cfg, "K": K, "variant": variant, "L": L, "error": str(e)}), flush=True)
