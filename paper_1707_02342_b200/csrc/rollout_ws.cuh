@@ -68,9 +68,9 @@ struct WsSmem {
 // SW = false reads them from the kernel-parameter constant bank (LDCU into
 // uniform registers).
 template <int H, int L, int Mode, bool SW>
-__global__ void __launch_bounds__(32 * L) rollout_ws_kernel(const __grid_constant__ RolloutArgs<float> a,
+__global__ void __launch_bounds__(32 * L, 1) rollout_ws_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const __grid_constant__ WeightHolder<float, H> wh) {
-  static_assert(H % (2 * L) == 0, "each role owns an even number of hidden units");
+  static_assert(H % (4 * L) == 0, "each role owns a multiple of 4 hidden units");
   constexpr int U = H / L;            // hidden units per role
   constexpr int kNoiseRole = (L > 1) ? 1 : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -191,12 +191,28 @@ __global__ void __launch_bounds__(32 * L) rollout_ws_kernel(const __grid_constan
     float2 acc[U / 2];
 #pragma unroll
     for (int p = 0; p < U / 2; ++p) acc[p] = *reinterpret_cast<const float2*>(&w.b2[role * U + 2 * p]);
+    {
+      // weight rows of own units as float4 (LDS.128 broadcast), double
+      // buffered one input ahead so the loads overlap the FFMA2s
+      constexpr int Q = U / 4;
+      const float4* W2 = reinterpret_cast<const float4*>(&w.w2t[0][role * U]);
+      float4 wb[2][Q];
 #pragma unroll
-    for (int i = 0; i < H; ++i) {
+      for (int q = 0; q < Q; ++q) wb[0][q] = W2[q];
 #pragma unroll
-      for (int p = 0; p < U / 2; ++p)
-        acc[p] = ffma2(*reinterpret_cast<const float2*>(&w.w2t[i][role * U + 2 * p]), make_float2(h1[i], h1[i]),
-                       acc[p]);
+      for (int i = 0; i < H; ++i) {
+        if (i + 1 < H) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) wb[(i + 1) & 1][q] = W2[(i + 1) * (H / 4) + q];
+        }
+        const float2 hh = make_float2(h1[i], h1[i]);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const float4 wv = wb[i & 1][q];
+          acc[2 * q] = ffma2(make_float2(wv.x, wv.y), hh, acc[2 * q]);
+          acc[2 * q + 1] = ffma2(make_float2(wv.z, wv.w), hh, acc[2 * q + 1]);
+        }
+      }
     }
 #pragma unroll
     for (int p = 0; p < U / 2; ++p) acc[p] = tanh2(acc[p]);
