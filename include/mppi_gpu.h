@@ -30,7 +30,7 @@
  *                       types.hpp:44-48; the quadratic test system uses 2.
  *       MLP weights     row-major W1 (H x 6), b1 (H), W2 (H x H), b2 (H),
  *                       W3 (4 x H), b3 (4) — the order of save_mlp,
- *                       dynamics.cpp:484-494.
+ *                       dynamics.cpp:297-307.
  *       costmap         row-major values[iy*width + ix], costs.hpp:11-38.
  *   - Fleet handles (n_controllers > 1) take per-controller arrays with a
  *     leading controller dimension (x0: n x state_dim, u0: n x 2).
@@ -49,7 +49,7 @@ extern "C" {
 
 /* Status codes.  The C++ wrapper maps them to the reference's exceptions:
  * INVALID_ARGUMENT and NONFINITE -> std::invalid_argument (types.hpp:105-122,
- * weights.cpp:10-12), RUNTIME -> std::runtime_error (dynamics.cpp:403-413). */
+ * weights.cpp:10-12), RUNTIME -> std::runtime_error (dynamics.cpp:216-225, IO). */
 enum {
   MPPI_OK = 0,
   MPPI_ERR_INVALID_ARGUMENT = 1,

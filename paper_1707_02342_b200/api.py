@@ -129,7 +129,7 @@ class MlpWeights:
         return w
 
     def save(self, path: str) -> None:
-        """save_mlp text format (dynamics.cpp:484-494), header ``6 H H 4``."""
+        """save_mlp text format (dynamics.cpp:297-307), header ``6 H H 4``."""
         H = self.hidden
         with open(path, "w") as f:
             f.write(f"6 {H} {H} 4\n")
@@ -140,7 +140,7 @@ class MlpWeights:
 
     @staticmethod
     def load(path: str, allowed_hidden: Sequence[int] = (32, 64)) -> "MlpWeights":
-        """load_mlp (dynamics.cpp:463-482); the reference accepts only 6 32 32 4."""
+        """load_mlp (dynamics.cpp:276-295); the reference accepts only 6 32 32 4."""
         try:
             with open(path) as f:
                 tok = f.read().split()

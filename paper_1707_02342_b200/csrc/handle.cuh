@@ -251,16 +251,21 @@ struct Handle final : HandleBase {
       return;
     }
     chunk_samples = 32;
-    // enough warps to cover the 148 x 4 sub-partitions several times over:
-    // L = clamp(pow2floor(2048 * 32 / K), 1, 8)
+    // Split the MLP over L warps until the grid holds ~1024 warps (measured
+    // on B200, tools/sweep.py: K=1920 -> L=4, K=16384 -> L=2, K>=65536 ->
+    // L=1; L=8 never won).  Weights: shared memory, except for the
+    // one-warp-per-chunk kernel at large K where the constant bank wins.
+    const long long chunks = (K + 31) / 32;
     int L = 1;
-    while (L < 8 && static_cast<long long>(2 * L) * K <= 2048LL * 32) L *= 2;
+    while (L < 4 && chunks * (2 * L) <= 1024) L *= 2;
+    if (H == 64 && L < 2) L = 2;  // the H = 64 kernels split the hidden layer over >= 2 warps
+    ws_smem_w = !(L == 1 && chunks >= 2048);
     if (const char* lv = std::getenv("MPPI_WS_L")) {
       const int want = std::atoi(lv);
       if (want == 1 || want == 2 || want == 4 || want == 8) L = want;
     }
     if (const char* sv = std::getenv("MPPI_WS_SMEM_W")) ws_smem_w = std::atoi(sv) != 0;
-    if (H == 64 && L < 2) L = 2;  // the H = 64 kernels split the hidden layer over >= 2 warps
+    if (H == 64 && L < 2) L = 2;
     ws_L = L;
   }
   void setup_merge() {

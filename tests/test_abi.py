@@ -109,3 +109,27 @@ def test_invalid_config_is_rejected_before_device_use():
     code = lib.mppi_gpu_create(ctypes.byref(cfg), ctypes.byref(h))
     assert code == _lib.MPPI_ERR_INVALID_ARGUMENT
     assert b"samples" in lib.mppi_gpu_last_error()
+
+
+def build_binding_check(tmp_dir):
+    """g++ the header-only C++ binding (include/mppi_gpu.hpp) against the library."""
+    exe = os.path.join(tmp_dir, "binding_check")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "binding_check.cpp"), "-L", libdir, "-lmppi_gpu",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    return exe
+
+
+@pytest.mark.skipif(api.device_count() > 0, reason="checks the no-device error path")
+def test_cpp_binding_exception_mapping(tmp_path):
+    out = subprocess.run([build_binding_check(str(tmp_path))], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "invalid_argument mapping ok" in out.stdout and "no-device runtime_error ok" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_binding_on_device(tmp_path):
+    out = subprocess.run([build_binding_check(str(tmp_path))], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "device binding ok" in out.stdout

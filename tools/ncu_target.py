@@ -9,7 +9,7 @@ from paper_1707_02342_b200 import workload  # noqa: E402
 from paper_1707_02342_b200.api import Controller  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
-K = int(sys.argv[2]) if len(sys.argv) > 2 else None
+K = (int(sys.argv[2]) or None) if len(sys.argv) > 2 else None
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 w = workload.make(cfg, samples=K)
 c = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox")
