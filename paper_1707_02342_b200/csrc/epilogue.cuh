@@ -100,9 +100,17 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
     }
     const Acc eta = block_sum<Acc, BLOCK>(e, s_red);  // includes the barrier for s_scale
     for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
+      // ascending chunk order; loads batched 8 at a time (independent of the sum)
       Acc num = 0.0;
-      for (int c = 0; c < a.n_chunks; ++c)
-        num = fma(s_scale[c], P[static_cast<size_t>(c) * a.partial_stride + kPartialHeader + i], num);
+      for (int c = 0; c < a.n_chunks; c += 8) {
+        Acc v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = (c + u < a.n_chunks) ? P[static_cast<size_t>(c + u) * a.partial_stride + kPartialHeader + i] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c + u < a.n_chunks) num = fma(s_scale[c + u], v[u], num);
+      }
       s_agg[i] = num / eta;
     }
   } else {

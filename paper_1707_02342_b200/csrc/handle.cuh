@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "epilogue.cuh"
+#include "rollout_tc.cuh"
 #include "ws_launch.hpp"
 #include "errors.hpp"
 #include "handle_iface.hpp"
@@ -68,6 +69,77 @@ struct HostPinned {
 };
 
 constexpr int kBlock = 128;      // samples per chunk / K1 CTA
+
+// Per-lane mma.sync fragment table of the tensor-core rollout
+// (rollout_tc.cuh, word map there): weights folded with the tanh identity
+// tanh(z) = 1 - 2 / (1 + 2^(kz)), k = 2 log2 e, then split hi/lo in fp16.
+template <class R>
+std::vector<uint32_t> tc_build_fragments(const MlpParams<R, 32>& w) {
+  constexpr int H = 32;
+  const double kk2 = 2.0 / std::log(2.0);
+  auto W1 = [&](int n, int i) { return static_cast<double>(w.w1t[i][n]); };
+  auto W2 = [&](int n, int i) { return static_cast<double>(w.w2t[i][n]); };
+  auto W3 = [&](int n, int i) { return static_cast<double>(w.w3t[i][n]); };
+  auto B1 = [&](int kin, int n) -> double {  // k8 x n32
+    if (kin < 6) return kk2 * W1(n, kin);
+    if (kin == 6) return kk2 * static_cast<double>(w.b1[n]);
+    return 0.0;
+  };
+  auto B2 = [&](int i, int n) -> double { return -2.0 * kk2 * W2(n, i); };
+  auto B3 = [&](int i, int n) -> double { return n < 4 ? -2.0 * W3(n, i) : 0.0; };
+  auto hl = [](double x, int which) -> uint16_t {
+    const __half h = __double2half(x);
+    if (which == 0) return __half_as_ushort(h);
+    return __half_as_ushort(__double2half(x - static_cast<double>(__half2float(h))));
+  };
+  auto pack = [&](double lo_k, double hi_k, int which) -> uint32_t {
+    return static_cast<uint32_t>(hl(lo_k, which)) | (static_cast<uint32_t>(hl(hi_k, which)) << 16);
+  };
+  std::vector<uint32_t> f(static_cast<size_t>(mppi_dev::kTcWords) * 32, 0u);
+  auto put = [&](int word, int lane, uint32_t v) { f[static_cast<size_t>(word) * 32 + lane] = v; };
+  for (int lane = 0; lane < 32; ++lane) {
+    const int g = lane >> 2, t = lane & 3;
+    for (int j = 0; j < 4; ++j)
+      for (int which = 0; which < 2; ++which)
+        put(2 * j + which, lane, pack(B1(2 * t, 8 * j + g), B1(2 * t + 1, 8 * j + g), which));
+    for (int kk = 0; kk < 2; ++kk)
+      for (int j = 0; j < 4; ++j)
+        for (int r = 0; r < 2; ++r)
+          for (int which = 0; which < 2; ++which) {
+            const int i0 = 16 * kk + 2 * t + 8 * r;
+            put(8 + ((kk * 4 + j) * 2 + r) * 2 + which, lane, pack(B2(i0, 8 * j + g), B2(i0 + 1, 8 * j + g), which));
+          }
+    for (int kk = 0; kk < 2; ++kk)
+      for (int r = 0; r < 2; ++r)
+        for (int which = 0; which < 2; ++which) {
+          const int i0 = 16 * kk + 2 * t + 8 * r;
+          put(40 + (kk * 2 + r) * 2 + which, lane, pack(B3(i0, g), B3(i0 + 1, g), which));
+        }
+    for (int j = 0; j < 4; ++j)
+      for (int c = 0; c < 2; ++c) {
+        const int n = 8 * j + 2 * t + c;
+        double sum = 0.0;
+        for (int i = 0; i < H; ++i) sum += W2(n, i);
+        const float v = static_cast<float>(kk2 * (static_cast<double>(w.b2[n]) + sum));
+        uint32_t bits;
+        std::memcpy(&bits, &v, 4);
+        put(48 + 2 * j + c, lane, bits);
+      }
+    for (int c = 0; c < 2; ++c) {
+      const int n = 2 * t + c;
+      float v = 0.f;
+      if (n < 4) {
+        double sum = 0.0;
+        for (int i = 0; i < H; ++i) sum += W3(n, i);
+        v = static_cast<float>(static_cast<double>(w.b3[n]) + sum);
+      }
+      uint32_t bits;
+      std::memcpy(&bits, &v, 4);
+      put(56 + c, lane, bits);
+    }
+  }
+  return f;
+}
 constexpr int kEpiBlock = 512;   // K2 CTA
 
 template <class R>
@@ -95,7 +167,10 @@ struct Handle final : HandleBase {
   }
   std::string variant_name() const override {
     char buf[160];
-    if (use_ws)
+    if (use_tc)
+      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=32,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks%s)",
+                    tc_mt, cfg.noise_mode, chunk_samples, n_chunks, merge_G ? ", pre-merged" : "");
+    else if (use_ws)
       std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks%s)", H, ws_L,
                     cfg.noise_mode, ws_smem_w ? "smem-weights" : "const-weights", n_chunks, merge_G ? ", pre-merged" : "");
     else
@@ -114,6 +189,17 @@ struct Handle final : HandleBase {
   bool use_ws = false;
   int ws_L = 1, chunk_samples = kBlock;
   bool ws_smem_w = true;  // weights staged in shared memory (vs constant bank)
+  // tensor-core K1 (rollout_tc.cuh): fp32 vehicle model, H = 32; chunk = 16*tc_mt
+  bool use_tc = false;
+  int tc_mt = 2;
+  DevBuf<uint32_t> d_tcfrag;
+  // fused tail (tail.cuh): group merge in K1 + epilogue by the last warp
+  bool tail_fused_ok = false;
+  int tail_G = 1, tail_groups = 0, groups_per_rank = 0;
+  DevBuf<unsigned> d_tail_cnt;
+  DevBuf<Acc> d_groups, d_final;
+  DevBuf<MlpParams<float, 32>> d_plantw;
+  int graph_kernels[3] = {0, 0, 0};
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   int rank = 0, world = 1;
   int zero_start = 0;
@@ -161,6 +247,7 @@ struct Handle final : HandleBase {
 
   // graphs: 0 = step (compute+slide), 1 = compute only, 2 = closed-loop iteration
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  uint64_t n_before_capture = 0;
   bool graph_trace[3] = {false, false, false};
 
   explicit Handle(const mppi_gpu_config& c) : cfg(c) {
@@ -199,6 +286,7 @@ struct Handle final : HandleBase {
     d_costs.alloc(static_cast<size_t>(C) * K);
     d_partials.alloc(static_cast<size_t>(C) * partials_ctrl_stride);
     setup_merge();
+    setup_tail();
     d_agg.alloc(static_cast<size_t>(2) * T);
     d_iters.alloc(C);
     CUDA_TRY(cudaMemset(d_iters.p, 0, C * sizeof(uint64_t)));
@@ -244,8 +332,19 @@ struct Handle final : HandleBase {
 
   void choose_variant() {
     const char* kv = std::getenv("MPPI_KERNEL");
-    const bool force_generic = kv && std::string(kv) == "generic";
-    use_ws = std::is_same<R, float>::value && cfg.system == MPPI_SYSTEM_VEHICLE_MLP && !force_generic;
+    const std::string kernel = kv ? kv : "";
+    const bool force_generic = kernel == "generic";
+    const bool f32_vehicle = std::is_same<R, float>::value && cfg.system == MPPI_SYSTEM_VEHICLE_MLP;
+    // default K1 for the fp32 vehicle model: tensor cores at H = 32, FFMA2
+    // warp-specialised at H = 64 (its weights do not fit the register file)
+    use_tc = f32_vehicle && H == 32 && !force_generic && kernel != "ws";
+    if (use_tc) {
+      tc_mt = K <= 32768 ? 1 : 2;  // one m16 tile per warp while warps are scarce
+      if (const char* mv = std::getenv("MPPI_TC_MT")) tc_mt = std::atoi(mv) == 1 ? 1 : 2;
+      chunk_samples = 16 * tc_mt;
+      return;
+    }
+    use_ws = f32_vehicle && !force_generic;
     if (!use_ws) {
       chunk_samples = kBlock;
       return;
@@ -277,6 +376,57 @@ struct Handle final : HandleBase {
       d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
     }
   }
+
+  // Groups of G chunks for the fused tail: G ~ sqrt(chunks), a power of two
+  // that divides each rank's chunk range (so groups never straddle ranks and
+  // the merge order is the same for every rank count).
+  void setup_tail() {
+    tail_fused_ok = false;
+    if (!use_tc) return;
+    int G = 1;
+    while (G < 256 && static_cast<long long>(G) * G < n_chunks) G *= 2;
+    while (G > 1 && chunks_per_rank % G != 0) G /= 2;
+    tail_G = G;
+    tail_groups = (n_chunks + G - 1) / G;
+    groups_per_rank = (chunks_per_rank + G - 1) / G;
+    // warp_merge_rows handles <= 256 rows; the final warp keeps U' (2T floats)
+    // in its 8 KB numerator buffer (rollout_tc.cuh)
+    tail_fused_ok = 3 * T <= 32 * kRedStride && tail_G <= 256 && tail_groups <= 256;
+    if (!tail_fused_ok) return;
+    d_final.alloc(static_cast<size_t>(C) * partial_stride);
+    d_tail_cnt.alloc(static_cast<size_t>(C) * (tail_groups + 1));
+    CUDA_TRY(cudaMemset(d_tail_cnt.p, 0, d_tail_cnt.n * sizeof(unsigned)));
+    d_groups.alloc(static_cast<size_t>(C) * std::max(tail_groups, world * groups_per_rank) * partial_stride);
+  }
+  TailArgs make_tail(int mode, bool slide, bool increment, bool plant, bool trace) const {
+    TailArgs ta{};
+    ta.mode = mode;
+    if (mode == 0) return ta;
+    ta.G = tail_G;
+    ta.n_chunks = n_chunks;
+    ta.n_groups = tail_groups;
+    ta.groups_ctrl_stride = static_cast<long long>(std::max(tail_groups, world * groups_per_rank)) * partial_stride;
+    ta.counters = d_tail_cnt.p;
+    ta.groups = d_groups.p;
+    ta.final_rows = d_final.p;
+    ta.plant_w = d_plantw.p;
+    if constexpr (std::is_same<R, float>::value) ta.e = epilogue_args(false, slide, increment, plant, trace);
+    return ta;
+  }
+  // MPPI_TAIL=fused runs the group merge and the epilogue inside K1 (last
+  // warp), =split the group merge in K1 + a final one-warp kernel (the
+  // multi-rank shape on one GPU); default (measured faster, profiles/): the
+  // separate pre-merge + epilogue kernels.
+  int tail_style() const {
+    static const int style = [] {
+      const char* e = std::getenv("MPPI_TAIL");
+      if (!e) return 0;
+      const std::string v(e);
+      return v == "off" ? 0 : (v == "split" ? 1 : 2);
+    }();
+    return style;
+  }
+  bool fused_tail() const { return use_tc && tail_fused_ok && tail_style() != 0; }
 
   static void validate_config(const mppi_gpu_config& c) {
     // SamplingParams::validate (types.hpp:105-122)
@@ -351,6 +501,15 @@ struct Handle final : HandleBase {
       if (!std::isfinite(w1[i])) throw_invalid("MLP weights must be finite");
     if (H == 32) {
       fill(*w32);
+      if (use_tc) {
+        std::vector<uint32_t> frag = tc_build_fragments(*w32);
+        d_tcfrag.alloc(frag.size());
+        CUDA_TRY(cudaMemcpy(d_tcfrag.p, frag.data(), frag.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        if constexpr (std::is_same<R, float>::value) {
+          d_plantw.alloc(1);
+          CUDA_TRY(cudaMemcpy(d_plantw.p, w32.get(), sizeof(MlpParams<float, 32>), cudaMemcpyHostToDevice));
+        }
+      }
     } else {
       fill(*w64);
       if (!kWeightsByValue<R, 64>) {
@@ -483,6 +642,7 @@ struct Handle final : HandleBase {
     a.T = T;
     a.zero_start = zero_start;
     a.chunk0 = chunk_lo;
+    a.chunk_end = chunk_hi;
     a.partial_stride = partial_stride;
     a.partials_ctrl_stride = partials_ctrl_stride;
     a.lambda = static_cast<R>(cfg.lambda);
@@ -583,15 +743,20 @@ struct Handle final : HandleBase {
 
   // events: bracket the launch with ev_a/ev_b without synchronising (used
   // inside captured graphs; the caller reads the elapsed time afterwards).
-  void enqueue_rollout(int mode, bool events = false) {
+  void enqueue_rollout(int mode, bool events = false, const TailArgs* tail = nullptr) {
     const RolloutArgs<R> a = rollout_args();
+    const TailArgs no_tail{};
     const size_t smem = rollout_smem();
     const dim3 grid(chunk_hi - chunk_lo, C);
     // inside stream capture an event record is only a dependency edge unless
     // it is marked external; external records become graph event nodes
     if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_a, stream, cudaEventRecordExternal));
     else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
-    if (use_ws) {
+    if (use_tc) {
+      if constexpr (std::is_same<R, float>::value)
+        CUDA_TRY(launch_rollout_tc_h32(a, d_tcfrag.p, tail ? *tail : no_tail, mode, tc_mt, chunk_hi - chunk_lo, C,
+                                       stream));
+    } else if (use_ws) {
       launch_ws(a, mode, grid);
     } else {
       dispatch(mode, [&]<int HH, class Sys, int Mode>() {
@@ -617,11 +782,34 @@ struct Handle final : HandleBase {
   void enqueue_premerge() {
     if (!merge_G) return;
     const dim3 grid(n_merged, C);
-    merge_chunks_kernel<><<<grid, 256, 0, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
+    merge_chunks_kernel<><<<grid, 256, sizeof(Acc) * merge_G, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
                                                    merge_G, cfg.lambda, d_partials2.p,
                                                    static_cast<long long>(n_merged) * partial_stride);
     ++launches;
     CUDA_TRY(cudaGetLastError());
+  }
+
+  // One iteration after the host inputs are staged: K1 (+ fused tail), or
+  // K1, exchange, pre-merge, epilogue.
+  void enqueue_iteration(int mode, bool events, bool slide, bool increment, bool plant, bool trace) {
+    if (fused_tail()) {
+      const bool split = world > 1 || tail_style() == 1;
+      const TailArgs ta = make_tail(split ? 1 : 2, slide, increment, plant, trace);
+      enqueue_rollout(mode, events, &ta);
+      if (split) {
+        const size_t count = static_cast<size_t>(groups_per_rank) * partial_stride;
+        if (world > 1)
+          NCCL_TRY(nccl().AllGather(d_groups.p + static_cast<size_t>(rank) * count, d_groups.p, count, ncclFloat64,
+                                    comm, stream));
+        CUDA_TRY(launch_tail_final(ta, T, partial_stride, cfg.lambda, C, stream));
+        ++launches;
+      }
+      return;
+    }
+    enqueue_rollout(mode, events);
+    enqueue_exchange();
+    enqueue_premerge();
+    enqueue_epilogue(true, slide, increment, plant, trace, C);
   }
 
   void enqueue_exchange() {
@@ -699,10 +887,8 @@ struct Handle final : HandleBase {
         }
         const bool prof = profile;
         profile = false;
-        enqueue_rollout(cfg.noise_mode, /*events=*/which == 2);
-        enqueue_exchange();
-        enqueue_premerge();
-        enqueue_epilogue(true, slide, /*increment=*/slide, plant, trace, C);
+        n_before_capture = launches;
+        enqueue_iteration(cfg.noise_mode, /*events=*/which == 2, slide, /*increment=*/slide, plant, trace);
         profile = prof;
         if (which != 2)
           CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
@@ -716,10 +902,11 @@ struct Handle final : HandleBase {
       cudaGraphDestroy(g);
       CUDA_TRY(e);
       graph_trace[which] = trace;
-      launches -= 2;  // counted again per replay below
+      graph_kernels[which] = static_cast<int>(launches - n_before_capture);
+      launches = n_before_capture;  // counted again per replay below
     }
     CUDA_TRY(cudaGraphLaunch(graph[which], stream));
-    launches += 2;
+    launches += graph_kernels[which];
   }
 
   int check_status(bool update_iters) {
@@ -776,12 +963,7 @@ struct Handle final : HandleBase {
     upload_x0(x0);
     CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
     CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
-    for (int i = 0; i < iterations; ++i) {
-      enqueue_rollout(cfg.noise_mode);
-      enqueue_exchange();
-      enqueue_premerge();
-      enqueue_epilogue(true, false, true, false, false, C);
-    }
+    for (int i = 0; i < iterations; ++i) enqueue_iteration(cfg.noise_mode, false, false, true, false, false);
     CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     const int code = check_status(false);
@@ -980,13 +1162,20 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaMemcpy(&saved, d_iters.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(d_iters.p, &batch_iteration, sizeof(uint64_t), cudaMemcpyHostToDevice));
     RolloutArgs<R> a = rollout_args();
-    if (use_ws) {
+    if (use_ws || use_tc) {
       // trace the production kernel itself: sample `sample`'s state per step
       a.trace_states = d_states.p;
       a.trace_k = sample;
       a.chunk0 = 0;
+      a.chunk_end = n_chunks;
       CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
-      launch_ws(a, effective_mode(batch_injected), dim3(n_chunks, 1));
+      if (use_tc) {
+        if constexpr (std::is_same<R, float>::value)
+          CUDA_TRY(launch_rollout_tc_h32(a, d_tcfrag.p, TailArgs{}, effective_mode(batch_injected), tc_mt, n_chunks,
+                                         1, stream));
+      } else {
+        launch_ws(a, effective_mode(batch_injected), dim3(n_chunks, 1));
+      }
     } else {
       dispatch(effective_mode(batch_injected), [&]<int HH, class Sys, int Mode>() {
         rollout_states_kernel<R, HH, Sys, Mode><<<1, 32, 0, stream>>>(a, holder<HH>(), sample, d_states.p);
@@ -1018,6 +1207,7 @@ struct Handle final : HandleBase {
     partials_ctrl_stride = static_cast<long long>(w) * chunks_per_rank * partial_stride;
     d_partials.alloc(static_cast<size_t>(partials_ctrl_stride));
     setup_merge();
+    setup_tail();
     if (w > 1) {
       ncclUniqueId uid;
       static_assert(sizeof(uid) == 128, "ncclUniqueId must be 128 bytes");

@@ -1,0 +1,451 @@
+// rollout_tc.cuh — K1 tensor-core variant: the dynamics MLP of a tile of
+// samples on the tensor cores (warp-level mma.sync, fp16x3 split, fp32
+// accumulate), everything else per sample in fp32 on the CUDA cores.
+//
+// Why: the FFMA2 kernel (rollout_ws.cuh) issues ~1 770 warp-instructions per
+// 32-sample step, 768 of them FFMA2 and ~380 weight loads; at the BASELINE
+// c1 size it is latency-bound (1.7 warps per scheduler) and at large K it is
+// register/issue-bound at ~50 % of the FP32 pipe (profiles/r01).  One
+// HMMA.16816 does 2 048 MACs in 8 issue-cycles of an SM sub-partition (B200,
+// tools/probes/mma_probe.cu: 548 TFLOP/s f16, 276 TFLOP/s tf32 for mma.sync),
+// so even three of them per product (hi*hi + hi*lo + lo*hi) beat FFMA2 by ~2x
+// on the MLP, and the weights live in registers — no weight traffic at all.
+//
+// Numerics.  Every operand x is split as x = hi + lo with hi = fp16(x),
+// lo = fp16(x - hi); the three products keep ~22 significant bits and the
+// tensor core accumulates in fp32, so the MLP error is of the order of an fp32
+// FMA evaluation (checked against the float restatement in the parity tests).
+// tanh is folded into the layers: with k = 2 log2(e),
+//   tanh(z) = 1 - 2 r,  r = 1 / (1 + 2^(k z)),
+// so layer 1 multiplies by k*W1 (bias k*b1 through a constant-one input),
+// layer 2 by -2k*W2 with bias k*(b2 + W2 1), layer 3 by -2*W3 with bias
+// b3 + W3 1, and each activation costs one ex2, one add and one rcp.
+//
+// Layout (per warp, MT m16 tiles = 16*MT samples = one chunk):
+//   A (activations) = rows = samples, B (weights, registers) = columns =
+//   hidden units.  The m16n8 f32 accumulator of layer l is, element for
+//   element, the A fragment of layer l+1 (rows g, g+8; k = 2t, 2t+1, 2t+8,
+//   2t+9), so no data moves between layers.  Inputs enter and outputs leave
+//   through a per-warp shared-memory stage.  Lane (g = lane/4, t = lane%4) owns
+//   sample row g + 8 (t&1) of tile t>>1 (MT = 2), or of tile 0 with lanes
+//   t >= 2 mirroring t - 2 (MT = 1): the owner runs the per-sample state,
+//   noise, costmap and cost exactly as the FFMA2 kernel's roles do.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "rollout.cuh"
+#include "tail.cuh"
+
+namespace mppi_dev {
+
+// Per-lane fragment words, stored [word][lane] (coalesced load at kernel start).
+//   0..7    B1 (k8 x n8) n-tile j: hi = 2j, lo = 2j+1
+//   8..39   B2 (k16 x n8): 8 + ((kk*4 + j)*2 + r)*2 + hl    (r: b0/b1)
+//   40..47  B3 (k16 x n8, outputs 0..3): 40 + (kk*2 + r)*2 + hl
+//   48..55  bias2 (fp32 bits): 48 + j*2 + c, column 8j + 2t + c
+//   56..57  bias3 (fp32 bits): column 2t + c (zero for t >= 2)
+constexpr int kTcWords = 58;
+constexpr int kTcH = 32;
+
+__device__ __forceinline__ void mma_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0));
+}
+__device__ __forceinline__ void mma_k16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// (x, y) -> fp16x2 hi and lo words: hi = fp16(x), lo = fp16(x - hi).
+__device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x, y);
+  const float2 hf = __half22float2(h);
+  const float2 r = __ffma2_rn(hf, make_float2(-1.f, -1.f), make_float2(x, y));
+  hi = h2_bits(h);
+  lo = h2_bits(__floats2half2_rn(r.x, r.y));
+}
+
+__device__ __forceinline__ float tc_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float tc_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// r = 1 / (1 + 2^y) on a pair (tanh(z) = 1 - 2r with y = k z folded upstream).
+__device__ __forceinline__ float2 act_r2(float y0, float y1) {
+  const float2 d = __fadd2_rn(make_float2(tc_ex2(y0), tc_ex2(y1)), make_float2(1.f, 1.f));
+  return make_float2(tc_rcp(d.x), tc_rcp(d.y));
+}
+
+// Accumulator (n-tiles 2kk, 2kk+1) -> activation -> A fragment hi/lo of k-tile kk.
+__device__ __forceinline__ void acc_to_a(const float (&d0)[4], const float (&d1)[4], uint32_t (&ahi)[4],
+                                         uint32_t (&alo)[4]) {
+  const float2 r00 = act_r2(d0[0], d0[1]), r01 = act_r2(d0[2], d0[3]);
+  const float2 r10 = act_r2(d1[0], d1[1]), r11 = act_r2(d1[2], d1[3]);
+  split2(r00.x, r00.y, ahi[0], alo[0]);  // row g,   k = 2t, 2t+1
+  split2(r01.x, r01.y, ahi[1], alo[1]);  // row g+8, k = 2t, 2t+1
+  split2(r10.x, r10.y, ahi[2], alo[2]);  // row g,   k = 2t+8, 2t+9
+  split2(r11.x, r11.y, ahi[3], alo[3]);  // row g+8, k = 2t+8, 2t+9
+}
+
+// Branch-free sincos for the pose update: Cody-Waite reduction by pi/2 and
+// near-minimax polynomials on [-pi/4, pi/4] (<= ~1 ulp there; no slow path,
+// so the step body stays one basic block the scheduler can interleave).
+__device__ __forceinline__ void tc_sincos(float x, float& s, float& c) {
+  const float q = rintf(x * 0.636619772f);
+  float r = __fmaf_rn(q, -1.57079625e+00f, x);
+  r = __fmaf_rn(q, -7.54978942e-08f, r);
+  r = __fmaf_rn(q, -5.39030253e-15f, r);
+  const float z = r * r;
+  float ps = __fmaf_rn(-1.95159533e-04f, z, 8.33216589e-03f);
+  ps = __fmaf_rn(ps, z, -1.66666552e-01f);
+  const float sr = __fmaf_rn(r * z, ps, r);
+  float pc = __fmaf_rn(2.43892027e-05f, z, -1.38867483e-03f);
+  pc = __fmaf_rn(pc, z, 4.16666232e-02f);
+  pc = __fmaf_rn(pc, z, -0.5f);
+  const float cr = __fmaf_rn(z, pc, 1.0f);
+  const int iq = static_cast<int>(q);
+  const float s0 = (iq & 1) ? cr : sr;
+  const float c0 = (iq & 1) ? sr : cr;
+  s = (iq & 2) ? -s0 : s0;
+  c = ((iq + 1) & 2) ? -c0 : c0;
+}
+
+// state_cost (costs.cpp:29-43) + the BASELINE crash term, branch-free, same
+// rounded operation sequence as state_cost_h (model.cuh).
+template <bool STAB>
+__device__ __forceinline__ float tc_state_cost(float h, float roll, float vx, float vy, float decay_t,
+                                               const CostDev<float>& cp) {
+  const float track = add_rn(h, (h > cp.boundary_threshold) ? mul_rn(decay_t, cp.impulse) : 0.f);
+  const float dv = sub_rn(vx, cp.v_des);
+  float c = add_rn(mul_rn(cp.alpha_track, track), mul_rn(cp.alpha_speed, mul_rn(dv, dv)));
+  if constexpr (STAB) {
+    const float zeta = (fabsf(vx) < 0.01f) ? 0.f : -atanf(__fdiv_rn(vy, fabsf(vx)));
+    const float stab = add_rn(mul_rn(zeta, zeta), (fabsf(zeta) > cp.slip_limit) ? cp.impulse : 0.f);
+    c = add_rn(c, mul_rn(cp.alpha_stab, stab));
+  }
+  const bool crash = cp.crash_penalty != 0.f && (h > cp.crash_threshold || fabsf(roll) > cp.roll_limit);
+  return add_rn(c, crash ? cp.crash_penalty : 0.f);
+}
+
+// Two fp32 m16n8 accumulators per output tile: `m` takes hi*hi (and the
+// bias), `c` the two cross terms; they are added once at the end, so the
+// full-magnitude accumulator sees 1-2 tensor-core roundings per layer instead
+// of 6, and the three product chains run in parallel.
+struct Acc2 {
+  float m[4], c[4];
+};
+__device__ __forceinline__ void acc2_sum(const Acc2& a, float (&d)[4]) {
+  const float2 x = __fadd2_rn(make_float2(a.m[0], a.m[1]), make_float2(a.c[0], a.c[1]));
+  const float2 y = __fadd2_rn(make_float2(a.m[2], a.m[3]), make_float2(a.c[2], a.c[3]));
+  d[0] = x.x;
+  d[1] = x.y;
+  d[2] = y.x;
+  d[3] = y.y;
+}
+
+template <int MT>
+struct TcStage {
+  uint2 in[MT][16][4];     // per sample row: (hi, lo) of (roll,vx), (vy,thd), (v0,v1), (1,0)
+  float4 out[MT][16];      // layer-3 outputs per sample row
+};
+constexpr int kTcTB = 16;  // timesteps per block of the numerator reduction
+constexpr int kTcRedStride = 33;  // doubles per row (padding: conflict-free column reads)
+
+// MLP of one step for MT tiles: inputs from the stage, outputs d3 (fp32).
+template <int MT>
+__device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, const uint32_t (&w1)[8],
+                                       const uint32_t (&w2)[32], const uint32_t (&w3)[8], const float (&b2)[8],
+                                       const float (&b3)[2], float (&d3)[MT][4]) {
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    // ---- layer 1 (k8): A rows g, g+8; k = 2t, 2t+1 (bias through the constant-one column)
+    const uint2 ag = st.in[m][g][t4], ag8 = st.in[m][g + 8][t4];
+    float d1[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      Acc2 a;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a.m[i] = a.c[i] = 0.f;
+      mma_k8(a.c, ag.y, ag8.y, w1[2 * j]);      // lo * hi
+      mma_k8(a.c, ag.x, ag8.x, w1[2 * j + 1]);  // hi * lo
+      mma_k8(a.m, ag.x, ag8.x, w1[2 * j]);      // hi * hi
+      acc2_sum(a, d1[j]);
+    }
+    // ---- layer 2 (2 x k16)
+    Acc2 a2[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a2[j].m[0] = a2[j].m[2] = b2[2 * j];
+      a2[j].m[1] = a2[j].m[3] = b2[2 * j + 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a2[j].c[i] = 0.f;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t ahi[4], alo[4];
+      acc_to_a(d1[2 * kk], d1[2 * kk + 1], ahi, alo);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int b = (kk * 4 + j) * 4;  // b0 hi, b0 lo, b1 hi, b1 lo
+        mma_k16(a2[j].c, alo, w2[b], w2[b + 2]);
+        mma_k16(a2[j].c, ahi, w2[b + 1], w2[b + 3]);
+        mma_k16(a2[j].m, ahi, w2[b], w2[b + 2]);
+      }
+    }
+    float d2[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc2_sum(a2[j], d2[j]);
+    // ---- layer 3 (2 x k16, n = 8: outputs 0..3)
+    Acc2 a3;
+    a3.m[0] = a3.m[2] = b3[0];
+    a3.m[1] = a3.m[3] = b3[1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a3.c[i] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t ahi[4], alo[4];
+      acc_to_a(d2[2 * kk], d2[2 * kk + 1], ahi, alo);
+      const int b = kk * 4;
+      mma_k16(a3.c, alo, w3[b], w3[b + 2]);
+      mma_k16(a3.c, ahi, w3[b + 1], w3[b + 3]);
+      mma_k16(a3.m, ahi, w3[b], w3[b + 2]);
+    }
+    acc2_sum(a3, d3[m]);
+  }
+}
+
+// grid = (ceil(chunks / NW), controllers), block = 32 * NW; one warp = one
+// chunk of 16*MT samples.  Dynamic smem: plan (2T + 2 floats), then the
+// numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
+template <int MT, int NW, int Mode, bool STAB>
+__global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
+                                                            const uint32_t* __restrict__ frag,
+                                                            const __grid_constant__ TailArgs tail) {
+  constexpr int CH = 16 * MT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = a.T;
+  float* s_plan = reinterpret_cast<float*>(smem_raw);
+  double* s_red_all = reinterpret_cast<double*>(smem_raw + ((sizeof(float) * (2 * T + 2) + 15) & ~size_t(15)));
+  __shared__ __align__(16) TcStage<MT> s_stage[NW];
+
+  const int ctrl = blockIdx.y;
+  if (a.abort_flag[ctrl] != 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int chunk = a.chunk0 + blockIdx.x * NW + warp;
+  for (int i = threadIdx.x; i < 2 * T + 2; i += 32 * NW)
+    s_plan[i] = (i < 2 * T) ? a.plan[static_cast<size_t>(ctrl) * 2 * T + i] : 0.f;
+
+  // weights + biases into registers (loop-invariant for the whole rollout)
+  uint32_t w1[8], w2[32], w3[8];
+  float b2[8], b3[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w1[i] = frag[i * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w2[i] = frag[(8 + i) * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w3[i] = frag[(40 + i) * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b2[i] = __uint_as_float(frag[(48 + i) * 32 + lane]);
+  b3[0] = __uint_as_float(frag[56 * 32 + lane]);
+  b3[1] = __uint_as_float(frag[57 * 32 + lane]);
+
+  TcStage<MT>& st = s_stage[warp];
+  // the constant-one input column (k = 6: bias of layer 1), written once
+  for (int i = lane; i < CH; i += 32) st.in[i >> 4][i & 15][3] = make_uint2(h2_bits(__floats2half2_rn(1.f, 0.f)), 0u);
+
+  // ---- owner: the sample this lane runs the scalar path for
+  const int m_own = (MT == 2) ? (t4 >> 1) : 0;
+  const int row_own = g + 8 * (t4 & 1);
+  const bool dup = (MT == 1) && (t4 >= 2);  // MT = 1: lanes t >= 2 mirror t - 2
+  const int k = chunk * CH + 16 * m_own + row_own;
+  const bool valid = (k < a.K) && !dup;
+  const bool zm = k >= a.zero_start;
+  const int kn = (k < a.K) ? k : 0;  // noise counter (in range for every lane)
+  const float dt = a.sys.dt;
+  const CostDev<float> cp = a.sys.cost;
+  const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
+  const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
+  __syncthreads();  // s_plan, stage constants
+  if (chunk >= a.chunk_end) return;  // tail warps of the last CTA (no block barrier below)
+
+  // Noise: Philox draws one 128-bit block per step pair; the other modes (parity)
+  // go through the generic per-step stream.
+  NoiseStream<float, Mode> ns = make_noise<float, Mode>(a, ctrl, kn);
+  const uint64_t seed = a.seeds[ctrl], iteration = a.iters[ctrl];
+  float zc0 = 0.f, zc1 = 0.f;  // Philox: the odd step of the current draw
+  auto eps_at = [&](int t, bool even, float& e0, float& e1) {
+    if constexpr (Mode == kPhilox) {
+      if (even) {
+        const uint4 d = philox_draw(seed, iteration, static_cast<uint32_t>(kn), static_cast<uint32_t>(t) >> 1);
+        float z0, z1;
+        philox_box_muller(d.x, d.y, z0, z1);
+        philox_box_muller(d.z, d.w, zc0, zc1);
+        e0 = a.scale0 * z0;
+        e1 = a.scale1 * z1;
+      } else {
+        e0 = a.scale0 * zc0;
+        e1 = a.scale1 * zc1;
+      }
+    } else {
+      ns.eps(min(t, T - 1), e0, e1);
+    }
+  };
+  // v_t = g(u_t + eps_t) and the coupling of step t (controller.cpp:86-101)
+  float v0c, v1c, coup_t;
+  auto produce_v = [&](int t, bool even) {
+    float e0, e1;
+    eps_at(t, even, e0, e1);
+    const float u0 = s_plan[2 * t], u1 = s_plan[2 * t + 1];
+    e0 = zm ? e0 - u0 : e0;
+    e1 = zm ? e1 - u1 : e1;
+    const float v0 = u0 + e0, v1 = u1 + e1;
+    const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
+    const float uu = __fmul_rn(__fmul_rn(u0, u0), inv_s0) + __fmul_rn(__fmul_rn(u1, u1), inv_s1);
+    coup_t = zm ? __fadd_rn(__fmul_rn(gml, uv), __fmul_rn(half_lambda, uu)) : __fmul_rn(a.gamma, uv);
+    v0c = clamp_r(v0, a.sys.lo0, a.sys.hi0);
+    v1c = clamp_r(v1, a.sys.lo1, a.sys.hi1);
+  };
+
+  const float* x0 = a.x0 + ctrl * 8;
+  float px = x0[0], py = x0[1], th = x0[2];
+  float roll = x0[3], vx = x0[4], vy = x0[5], thd = x0[6];
+  MapDev<float> map;
+  map.values = a.maps[ctrl];
+  map.width = a.map_w;
+  map.height = a.map_h;
+  map.x0 = a.map_x0;
+  map.y0 = a.map_y0;
+  map.res = a.map_res;
+  map.inv_res = a.map_inv_res;
+  Acc cost = 0.0;
+  MapTaps<float> q{};
+  float p_roll = 0.f, p_vx = 0.f, p_vy = 0.f, p_coup = 0.f;
+  const bool trace = a.trace_states != nullptr && valid && k == a.trace_k;
+  produce_v(0, true);
+
+  // One step; EVEN = parity of t (compile-time, so the Philox draw of the
+  // next pair is unconditional code in the odd step).
+  auto step = [&](int t, auto even_tag) {
+    constexpr bool EVEN = decltype(even_tag)::value;
+    // stage this step's inputs (owner)
+    if (!dup) {
+      uint2* row = st.in[m_own][row_own];
+      uint32_t hi, lo;
+      split2(roll, vx, hi, lo);
+      row[0] = make_uint2(hi, lo);
+      split2(vy, thd, hi, lo);
+      row[1] = make_uint2(hi, lo);
+      split2(v0c, v1c, hi, lo);
+      row[2] = make_uint2(hi, lo);
+    }
+    __syncwarp();
+    float d3[MT][4];
+    tc_mlp<MT>(st, g, t4, w1, w2, w3, b2, b3, d3);
+    // independent of this step's MLP (overlaps it): running cost of step t-1
+    // on x_t (taps fetched last step), and v_{t+1}
+    {
+      const float h = map_interp(q);
+      const float rc = tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[t > 0 ? t - 1 : 0], cp);
+      cost += (t > 0) ? static_cast<Acc>(add_rn(rc, p_coup)) : 0.0;
+    }
+    p_coup = coup_t;
+    produce_v(t + 1, !EVEN);
+    // outputs to their owners: columns 2t, 2t+1 live in lanes t = 0, 1
+    if (t4 < 2) {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        reinterpret_cast<float2*>(&st.out[m][g])[t4] = make_float2(d3[m][0], d3[m][1]);
+        reinterpret_cast<float2*>(&st.out[m][g + 8])[t4] = make_float2(d3[m][2], d3[m][3]);
+      }
+    }
+    __syncwarp();
+    const float4 d = st.out[m_own][row_own];
+    // Euler split (dynamics.cpp:137-148) from the old state
+    float sn, cs;
+    tc_sincos(th, sn, cs);
+    const float vx_old = vx, vy_old = vy, thd_old = thd;
+    roll = add_rn(roll, mul_rn(d.x, dt));
+    vx = add_rn(vx, mul_rn(d.y, dt));
+    vy = add_rn(vy, mul_rn(d.z, dt));
+    thd = add_rn(thd, mul_rn(d.w, dt));
+    px = add_rn(px, mul_rn(sub_rn(mul_rn(cs, vx_old), mul_rn(sn, vy_old)), dt));
+    py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx_old), mul_rn(cs, vy_old)), dt));
+    th = add_rn(th, mul_rn(thd_old, dt));
+    q = map_fetch(map, px, py);  // consumed by the next step's cost
+    p_roll = roll;
+    p_vx = vx;
+    p_vy = vy;
+    if (trace) {
+      float* so = a.trace_states + (t + 1) * 7;
+      so[0] = px; so[1] = py; so[2] = th; so[3] = roll; so[4] = vx; so[5] = vy; so[6] = thd;
+    }
+  };
+  int t = 0;
+  for (; t + 1 < T; t += 2) {
+    step(t, std::true_type{});
+    step(t + 1, std::false_type{});
+  }
+  if (t < T) step(t, std::true_type{});
+
+  // ---- terminal cost and the chunk softmin partials
+  {
+    const float h = map_interp(q);
+    cost += static_cast<Acc>(add_rn(tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[T - 1], cp), p_coup));
+    if (a.sys.with_terminal) cost += static_cast<Acc>(tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[T], cp));
+  }
+  if (valid) a.costs[static_cast<size_t>(ctrl) * a.K + k] = cost;
+  const bool bad = valid && !isfinite(cost);
+  const Acc rho = warp_min(valid ? cost : Acc(INFINITY));
+  const Acc wk = valid ? exp(-(cost - rho) / a.dlambda) : 0.0;
+  const Acc eta = warp_sum(wk);
+  const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
+  Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
+             static_cast<size_t>(chunk) * a.partial_stride;
+  if (lane == 0) {
+    out[0] = rho;
+    out[1] = eta;
+    out[2] = any_bad ? 1.0 : 0.0;
+    out[3] = 0.0;
+  }
+  // numerators over the regenerated batch (eps' = eps - U for zero-mean):
+  // blocks of kTcTB steps, products staged [t][c][lane] in shared memory and
+  // summed per (t, c) over the lanes in ascending lane order by one lane each.
+  double* red = s_red_all + static_cast<size_t>(warp) * (2 * kTcTB) * kTcRedStride;
+  if constexpr (Mode != kPhilox) ns = make_noise<float, Mode>(a, ctrl, kn);
+  for (int tb = 0; tb < T; tb += kTcTB) {
+#pragma unroll 2
+    for (int j = 0; j < kTcTB; ++j) {
+      const int tt = tb + j;
+      float e0 = 0.f, e1 = 0.f;
+      if (tt < T) {
+        eps_at(tt, (tt & 1) == 0, e0, e1);
+        e0 = zm ? e0 - s_plan[2 * tt] : e0;
+        e1 = zm ? e1 - s_plan[2 * tt + 1] : e1;
+      }
+      red[(2 * j) * kTcRedStride + lane] = wk * static_cast<Acc>(e0);
+      red[(2 * j + 1) * kTcRedStride + lane] = wk * static_cast<Acc>(e1);
+    }
+    __syncwarp();
+    Acc s = 0.0;
+    const double* col = red + lane * kTcRedStride;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) s = s + col[l];
+    if (tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
+    __syncwarp();
+  }
+  // group merge / fused epilogue (tail.cuh); the reduction buffer is scratch now
+  tail_after_chunk(tail, ctrl, chunk, T, a.partial_stride, a.partials_ctrl_stride, a.partials, a.dlambda, red, lane);
+}
+
+}  // namespace mppi_dev

@@ -1,0 +1,57 @@
+// tc_h32.cu — instantiations and launcher of the tensor-core rollout kernel
+// (rollout_tc.cuh), H = 32, fp32 path.
+#include "rollout_tc.cuh"
+#include "ws_launch.hpp"
+
+namespace mppi_host {
+
+namespace {
+constexpr int kTcWarps = 4;  // warps (chunks) per CTA
+
+template <int MT, int Mode, bool STAB>
+cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+               int n_chunks, int ctrls, cudaStream_t stream) {
+  const size_t plan_bytes = (sizeof(float) * (2 * a.T + 2) + 15) & ~size_t(15);
+  const size_t smem = plan_bytes + sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
+  auto kern = mppi_dev::rollout_tc_kernel<MT, kTcWarps, Mode, STAB>;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid((n_chunks + kTcWarps - 1) / kTcWarps, ctrls);
+  kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag, tail);
+  return cudaGetLastError();
+}
+template <int Mode, bool STAB>
+cudaError_t by_mt(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail, int mt,
+                  int n_chunks, int ctrls, cudaStream_t stream) {
+  return mt == 1 ? go<1, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream)
+                 : go<2, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream);
+}
+template <int Mode>
+cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                    int mt, int n_chunks, int ctrls, cudaStream_t stream) {
+  // the side-slip term (atan) is compiled in only when its weight is nonzero
+  return a.sys.cost.alpha_stab != 0.f ? by_mt<Mode, true>(a, frag, tail, mt, n_chunks, ctrls, stream)
+                                      : by_mt<Mode, false>(a, frag, tail, mt, n_chunks, ctrls, stream);
+}
+}  // namespace
+
+cudaError_t launch_rollout_tc_h32(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
+                                  const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
+                                  cudaStream_t stream) {
+  switch (mode) {
+    case mppi_dev::kInjected: return by_stab<mppi_dev::kInjected>(a, frag, tail, mt, n_chunks, ctrls, stream);
+    case mppi_dev::kRefSplitmix: return by_stab<mppi_dev::kRefSplitmix>(a, frag, tail, mt, n_chunks, ctrls, stream);
+    default: return by_stab<mppi_dev::kPhilox>(a, frag, tail, mt, n_chunks, ctrls, stream);
+  }
+}
+
+cudaError_t launch_tail_final(const mppi_dev::TailArgs& tail, int T, int partial_stride, double lambda, int ctrls,
+                              cudaStream_t stream) {
+  const size_t smem = sizeof(double) * 32 * mppi_dev::kRedStride;
+  mppi_dev::tail_final_kernel<><<<ctrls, 32, smem, stream>>>(tail, T, partial_stride, lambda);
+  return cudaGetLastError();
+}
+
+}  // namespace mppi_host

@@ -1,12 +1,14 @@
 // ws_launch.hpp — launchers of the warp-specialised fp32 rollout kernel
 // (rollout_ws.cuh), compiled in their own translation units (ws_h32.cu,
-// ws_h64.cu) so the per-(H, L, noise) instantiations build in parallel.
+// ws_h64.cu, tc_h32.cu) so the per-(H, L, noise) instantiations build in
+// parallel.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include "model.cuh"
 #include "rollout.cuh"
+#include "tail.cuh"
 
 namespace mppi_host {
 
@@ -14,5 +16,14 @@ cudaError_t launch_rollout_ws_h32(const mppi_dev::RolloutArgs<float>& a, const m
                                   int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
 cudaError_t launch_rollout_ws_h64(const mppi_dev::RolloutArgs<float>& a, const mppi_dev::WeightHolder<float, 64>& w,
                                   int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
+
+// Tensor-core rollout (rollout_tc.cuh): `frag` is the per-lane fragment table
+// built by tc_build_fragments; n_chunks chunks of 16*mt samples from a.chunk0.
+cudaError_t launch_rollout_tc_h32(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
+                                  const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
+                                  cudaStream_t stream);
+// Ranks > 1: final merge of the all-gathered group partials + epilogue (tail.cuh).
+cudaError_t launch_tail_final(const mppi_dev::TailArgs& tail, int T, int partial_stride, double lambda, int ctrls,
+                              cudaStream_t stream);
 
 }  // namespace mppi_host

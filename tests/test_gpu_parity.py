@@ -19,6 +19,12 @@ pytestmark = pytest.mark.gpu
 COST_RTOL_FP32 = 1e-5
 WEIGHT_RTOL_FP32 = 1e-4
 PLAN_ATOL_FP32 = 1e-5
+# The tensor-core K1 (default fp32 path at H = 32) evaluates the MLP with a
+# different summation order than the float restatement (fp16x3 mma, fp32
+# accumulate), so one update agrees with it to 2.5e-5 rather than 1e-5; against
+# the double reference it must be no worse than fp32 arithmetic itself (the
+# float restatement differs from the double one by ~9e-5 per update at c0).
+PLAN_ATOL_FP32_VS_FLOAT_ORACLE = 2.5e-5
 
 
 def pair(w, precision, noise, cost=None, hidden=None, **kw):
@@ -183,8 +189,16 @@ def test_mpc_step_receding_horizon(prec, noise):
     """Fused K1 (rollout + chunk softmin partials) + K2 (merge, SG, update, slide) vs mpc_step."""
     w = c0()
     g, o = pair(w, prec, noise)
+    o64 = None
+    if prec == "fp32":
+        o64 = oracle.OracleController(w.params, w.bounds, w.sg, w.cost, hidden=32, precision="fp64", noise=noise)
+        o64.set_mlp(w.mlp)
+        o64.set_costmap(w.costmap)
     x = w.x0[0].copy()
     for it in range(5):
+        if o64 is not None:
+            o64.plan = o.plan
+            o64.iteration = o.iteration
         ud = g.mpc_step(x)
         uo = o.mpc_step(x, threads=8)
         pd, po = g.plan, o.plan
@@ -192,8 +206,14 @@ def test_mpc_step_receding_horizon(prec, noise):
             assert np.allclose(ud, uo, rtol=0, atol=1e-10), it
             assert np.allclose(pd, po, rtol=0, atol=1e-10), it
         else:
-            assert np.max(np.abs(pd - po)) <= PLAN_ATOL_FP32, (it, np.max(np.abs(pd - po)))
-            assert np.max(np.abs(ud - uo)) <= PLAN_ATOL_FP32
+            o64.mpc_step(x, threads=8)
+            ref = o64.plan
+            err_f, err_d = np.max(np.abs(pd - po)), np.max(np.abs(pd - ref))
+            err_oracle = np.max(np.abs(po - ref))  # fp32 arithmetic itself vs the double reference
+            tol = PLAN_ATOL_FP32_VS_FLOAT_ORACLE if "rollout_tc" in g.kernel_variant else PLAN_ATOL_FP32
+            assert err_f <= tol, (it, err_f)
+            assert err_d <= 1.25 * err_oracle + 1e-6, (it, err_d, err_oracle)
+            assert np.max(np.abs(ud - uo)) <= tol
             g.plan = po  # keep both on the same trajectory of plans
         assert g.iteration == o.iteration == it + 1
         x = o.vehicle_step(x, uo)
@@ -314,5 +334,52 @@ def test_kernel_variant_and_launch_count():
     g, _ = pair(w, "fp32", "philox")
     n0 = g.launch_count
     g.mpc_step(w.x0[0])
-    assert g.launch_count - n0 == 2  # K1 rollout + K2 epilogue
-    assert "rollout_ws_kernel" in g.kernel_variant  # the fp32 vehicle path is the warp-specialised K1
+    # the fp32 H = 32 vehicle path is the tensor-core K1 (+ the epilogue kernel)
+    assert "rollout_tc_kernel" in g.kernel_variant
+    assert g.launch_count - n0 == 2
+    w64 = workload.make("c2", samples=256, horizon_steps=20)
+    g64, _ = pair(w64, "fp32", "philox")
+    n0 = g64.launch_count
+    g64.mpc_step(w64.x0[0])
+    assert "rollout_ws_kernel" in g64.kernel_variant  # H = 64: the FFMA2 warp-specialised K1
+    assert g64.launch_count - n0 == 2  # K1 + epilogue
+
+
+_TAIL_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+from paper_1707_02342_b200 import workload
+from paper_1707_02342_b200.api import Controller
+w = workload.make('c1', samples=int(sys.argv[2]))
+g = Controller(w.params, w.bounds, w.sg, w.cost, hidden=32, precision='fp32', noise='philox')
+g.set_mlp(w.mlp); g.set_costmap(w.costmap)
+n0 = g.launch_count
+u = [g.mpc_step(w.x0[0]).tolist() for _ in range(3)]
+print(json.dumps({'plan': g.plan.tolist(), 'u': u, 'launches': g.launch_count - n0, 'it': g.iteration}))
+"""
+
+
+@pytest.mark.parametrize("K", [1920, 16384])
+def test_tail_styles_agree(K):
+    """The three tails of the tensor-core path (separate pre-merge + epilogue
+    kernels; group merge in K1 + one-warp final kernel = the multi-rank shape;
+    everything fused into K1's last warp) give the same plan: split and fused
+    run identical arithmetic (bit-equal), the kernel tail differs only in the
+    merge order (rounding)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for style in ("off", "split", "fused"):
+        env = dict(os.environ, MPPI_TAIL=style)
+        out = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, str(K)], env=env, capture_output=True,
+                             text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[style] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["fused"]["launches"] == 3 and res["split"]["launches"] == 6
+    assert res["fused"]["plan"] == res["split"]["plan"] and res["fused"]["u"] == res["split"]["u"]
+    assert np.max(np.abs(np.array(res["fused"]["plan"]) - np.array(res["off"]["plan"]))) <= 1e-6
+    assert all(r["it"] == 3 for r in res.values())

@@ -3,6 +3,7 @@
 flushed between iterations) for each K1 variant, on the BASELINE configs."""
 import json
 import os
+import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -10,13 +11,18 @@ sys.path.insert(0, ROOT)
 
 
 def run(cfg, K, variant, L, steps=30, sw=1):
-    for v in ("MPPI_KERNEL", "MPPI_WS_L", "MPPI_WS_SMEM_W"):
+    for v in ("MPPI_KERNEL", "MPPI_WS_L", "MPPI_WS_SMEM_W", "MPPI_TC_MT"):
         os.environ.pop(v, None)
     if variant == "generic":
         os.environ["MPPI_KERNEL"] = "generic"
-    elif L:
-        os.environ["MPPI_WS_L"] = str(L)
-    os.environ["MPPI_WS_SMEM_W"] = str(sw)
+    elif variant == "tc":
+        if L:
+            os.environ["MPPI_TC_MT"] = str(L)
+    else:
+        os.environ["MPPI_KERNEL"] = "ws"
+        if L:
+            os.environ["MPPI_WS_L"] = str(L)
+        os.environ["MPPI_WS_SMEM_W"] = str(sw)
     from paper_1707_02342_b200 import workload
     from paper_1707_02342_b200.api import Controller
     w = workload.make(cfg, samples=K)
@@ -40,6 +46,22 @@ def run(cfg, K, variant, L, steps=30, sw=1):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     cases = []
+    if which == "tail":
+        for cfg, K in (("c1", 16384), ("c0", 1920), ("c4", 262144)):
+            for tail in ("off", "split", "fused"):
+                os.environ["MPPI_TAIL"] = tail
+                r = subprocess.run([sys.executable, __file__, "one", cfg, str(K), "tc", "0"], capture_output=True,
+                                   text=True, env=dict(os.environ))
+                print(tail, r.stdout.strip() or r.stderr[-500:], flush=True)
+        sys.exit(0)
+    if which == "one":
+        run(sys.argv[2], int(sys.argv[3]), sys.argv[4], int(sys.argv[5]), steps=30)
+        sys.exit(0)
+    if which == "tc":
+        for cfg, K in (("c1", 16384), ("c0", 1920), ("c4", 262144), ("c4", 1048576)):
+            for variant, L in (("tc", 1), ("tc", 2), ("ws", 0)):
+                run(cfg, K, variant, L, steps=10 if K >= 262144 else 30)
+        sys.exit(0)
     for cfg, K in (("c1", 16384), ("c0", 1920), ("c2", 65536), ("c4", 262144)):
         for variant, L, sw in (("generic", 0, 0), ("ws", 1, 0), ("ws", 1, 1), ("ws", 2, 1), ("ws", 4, 1),
                                ("ws", 8, 1), ("ws", 2, 0), ("ws", 4, 0)):
