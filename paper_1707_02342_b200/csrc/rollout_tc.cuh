@@ -227,7 +227,7 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
 // grid = (ceil(chunks / NW), controllers), block = 32 * NW; one warp = one
 // chunk of 16*MT samples.  Dynamic smem: plan (2T + 2 floats), then the
 // numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
-template <int MT, int NW, int Mode, bool STAB>
+template <int MT, int NW, int Mode, bool STAB, bool STORE>
 __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const uint32_t* __restrict__ frag,
                                                             const __grid_constant__ TailArgs tail) {
@@ -236,6 +236,11 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const int T = a.T;
   float* s_plan = reinterpret_cast<float*>(smem_raw);
   double* s_red_all = reinterpret_cast<double*>(smem_raw + ((sizeof(float) * (2 * T + 2) + 15) & ~size_t(15)));
+  // STORE: the rollout keeps eps' (the batch as rollout_batch leaves it) of
+  // its samples on chip, [warp][t][sample] float2, for the numerator pass —
+  // used when the whole grid fits one wave with this footprint (small K);
+  // otherwise eps' is regenerated from the counters.
+  float2* s_eps_all = reinterpret_cast<float2*>(s_red_all + static_cast<size_t>(NW) * 2 * kTcTB * kTcRedStride);
   __shared__ __align__(16) TcStage<MT> s_stage[NW];
 
   const int ctrl = blockIdx.y;
@@ -303,12 +308,17 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   };
   // v_t = g(u_t + eps_t) and the coupling of step t (controller.cpp:86-101)
   float v0c, v1c, coup_t;
+  float2* s_eps = STORE ? s_eps_all + static_cast<size_t>(warp) * T * CH : nullptr;
+  const int s_own = 16 * m_own + row_own;
   auto produce_v = [&](int t, bool even) {
     float e0, e1;
     eps_at(t, even, e0, e1);
     const float u0 = s_plan[2 * t], u1 = s_plan[2 * t + 1];
     e0 = zm ? e0 - u0 : e0;
     e1 = zm ? e1 - u1 : e1;
+    if constexpr (STORE) {
+      if (t < T && !dup) s_eps[t * CH + s_own] = make_float2(e0, e1);
+    }
     const float v0 = u0 + e0, v1 = u1 + e1;
     const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
     const float uu = __fmul_rn(__fmul_rn(u0, u0), inv_s0) + __fmul_rn(__fmul_rn(u1, u1), inv_s1);
@@ -429,9 +439,15 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
       const int tt = tb + j;
       float e0 = 0.f, e1 = 0.f;
       if (tt < T) {
-        eps_at(tt, (tt & 1) == 0, e0, e1);
-        e0 = zm ? e0 - s_plan[2 * tt] : e0;
-        e1 = zm ? e1 - s_plan[2 * tt + 1] : e1;
+        if constexpr (STORE) {
+          const float2 ev = s_eps[tt * CH + s_own];
+          e0 = ev.x;
+          e1 = ev.y;
+        } else {
+          eps_at(tt, (tt & 1) == 0, e0, e1);
+          e0 = zm ? e0 - s_plan[2 * tt] : e0;
+          e1 = zm ? e1 - s_plan[2 * tt + 1] : e1;
+        }
       }
       red[(2 * j) * kTcRedStride + lane] = wk * static_cast<Acc>(e0);
       red[(2 * j + 1) * kTcRedStride + lane] = wk * static_cast<Acc>(e1);

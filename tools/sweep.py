@@ -54,6 +54,15 @@ if __name__ == "__main__":
                                    text=True, env=dict(os.environ))
                 print(tail, r.stdout.strip() or r.stderr[-500:], flush=True)
         sys.exit(0)
+    if which == "envs":
+        # python tools/sweep.py envs '[["c1",16384,{"MPPI_TC_STORE":"0"}], ...]'
+        for cfg, K, env in json.loads(sys.argv[2]):
+            e = dict(os.environ)
+            e.update(env)
+            r = subprocess.run([sys.executable, __file__, "one", cfg, str(K), "tc", "0"], capture_output=True,
+                               text=True, env=e)
+            print(json.dumps(env), r.stdout.strip() or r.stderr[-500:], flush=True)
+        sys.exit(0)
     if which == "one":
         run(sys.argv[2], int(sys.argv[3]), sys.argv[4], int(sys.argv[5]), steps=30)
         sys.exit(0)
