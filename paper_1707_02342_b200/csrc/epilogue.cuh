@@ -27,6 +27,7 @@ constexpr int kMaxSgWindow = 63;
 template <class R>
 struct EpilogueArgs {
   int T, n_chunks, partial_stride;
+  int tile_rows;                 // partial rows staged per shared-memory tile
   long long partials_ctrl_stride;
   double lambda;
   R lo0, lo1, hi0, hi1;
@@ -56,68 +57,95 @@ __device__ __forceinline__ int reflect_index(int i, int n) {
   return i;
 }
 
-// Dynamic smem: agg (2T, double) + chunk scale factors (n_chunks, double) +
-// U' (2T, R) + MLP scratch (2H, R).
+// Dynamic smem: agg (2T doubles) | chunk scales (n_chunks doubles) | a tile
+// of tile_rows partial rows (tile_rows x partial_stride doubles) | U' (2T R) |
+// MLP scratch (2H R) | the plant's MLP weights (MlpParams<R,H>, plant only).
+// The partial rows are merged tile by tile: every value of a tile is loaded
+// at once into shared memory (one L2 round trip per tile), then each thread
+// accumulates its elements over the rows in ascending order.
+template <class R, int H>
+__host__ __device__ constexpr size_t epilogue_smem_bytes(int T, int n_chunks, int tile_rows, int stride, bool plant) {
+  return sizeof(Acc) * (2 * T + n_chunks + static_cast<size_t>(tile_rows) * stride) + sizeof(R) * (2 * T + 2 * H) +
+         (plant ? sizeof(MlpParams<R, H>) + 16 : 0);
+}
 template <class R, int H, class Sys, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__ EpilogueArgs<R> a,
                                                          const __grid_constant__ WeightHolder<R, H> wh) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
+  const int n_rows = a.partials ? a.n_chunks : 0;
   Acc* s_agg = reinterpret_cast<Acc*>(smem_raw);
   Acc* s_scale = s_agg + 2 * T;
-  R* s_new = reinterpret_cast<R*>(s_scale + (a.partials ? a.n_chunks : 0));
+  Acc* s_tile = s_scale + n_rows;
+  R* s_new = reinterpret_cast<R*>(s_tile + (a.partials ? static_cast<size_t>(a.tile_rows) * a.partial_stride : 0));
   R* s_mlp = s_new + 2 * T;
+  MlpParams<R, H>* s_w = reinterpret_cast<MlpParams<R, H>*>(
+      (reinterpret_cast<uintptr_t>(s_mlp + 2 * H) + 15) & ~uintptr_t(15));
   __shared__ Acc s_red[BLOCK / 32];
   __shared__ int s_bad;
   __shared__ R s_u[2];
+  __shared__ Acc s_eta;
   const int ctrl = blockIdx.x;
   StepStatus* st = a.status + ctrl;
   if (st->code != 0) return;  // sticky abort: a previous stage failed
   R* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
+  if constexpr (Sys::kHasMap) {
+    if (a.plant) {  // stage the plant's weights (overlaps the merge)
+      const float4* src = reinterpret_cast<const float4*>(&wh.get());
+      float4* dst = reinterpret_cast<float4*>(s_w);
+      for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<R, H>) / 16); i += BLOCK) dst[i] = src[i];
+    }
+  }
 
   if (a.partials) {
     const Acc* P = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride;
+    const int stride = a.partial_stride;
     // any non-finite sample cost -> it_weights throws (weights.cpp:12)
     if (threadIdx.x == 0) s_bad = 0;
     __syncthreads();
     Acc m = INFINITY;
-    for (int c = threadIdx.x; c < a.n_chunks; c += BLOCK) {
-      const Acc* pc = P + static_cast<size_t>(c) * a.partial_stride;
+    for (int c = threadIdx.x; c < n_rows; c += BLOCK) {
+      const Acc* pc = P + static_cast<size_t>(c) * stride;
       if (pc[2] != 0.0) s_bad = 1;
-      m = (pc[0] < m) ? pc[0] : m;
+      const Acc r = pc[0];
+      m = (r < m) ? r : m;
+      s_scale[c] = r;
     }
     const Acc rho = block_min<Acc, BLOCK>(m, s_red);
     if (s_bad) {
       if (threadIdx.x == 0) st->code = 2;  // MPPI_ERR_NONFINITE
       return;
     }
-    Acc e = 0.0;
-    for (int c = threadIdx.x; c < a.n_chunks; c += BLOCK) {
-      const Acc* pc = P + static_cast<size_t>(c) * a.partial_stride;
-      const Acc s = exp(-(pc[0] - rho) / a.lambda);
-      s_scale[c] = s;
-      e = e + s * pc[1];
-    }
-    const Acc eta = block_sum<Acc, BLOCK>(e, s_red);  // includes the barrier for s_scale
-    for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
-      // ascending chunk order; loads batched 8 at a time (independent of the sum)
-      Acc num = 0.0;
-      for (int c = 0; c < a.n_chunks; c += 8) {
-        Acc v[8];
+    for (int c = threadIdx.x; c < n_rows; c += BLOCK) s_scale[c] = exp(-(s_scale[c] - rho) / a.lambda);
+    // per-thread accumulators: element 1 (eta) and the 2T numerators
+    constexpr int kMaxPer = (2 * 4096 + kPartialHeader + BLOCK - 1) / BLOCK;  // T <= 4096
+    Acc acc[kMaxPer];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          v[u] = (c + u < a.n_chunks) ? P[static_cast<size_t>(c + u) * a.partial_stride + kPartialHeader + i] : 0.0;
+    for (int q = 0; q < kMaxPer; ++q) acc[q] = 0.0;
+    for (int r0 = 0; r0 < n_rows; r0 += a.tile_rows) {
+      const int nr = min(a.tile_rows, n_rows - r0);
+      __syncthreads();  // previous tile consumed (and s_scale written)
+      const Acc* src = P + static_cast<size_t>(r0) * stride;
+      for (int f = threadIdx.x; f < nr * stride; f += BLOCK) s_tile[f] = src[f];
+      __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u < a.n_chunks) num = fma(s_scale[c + u], v[u], num);
+      for (int q = 0; q < kMaxPer; ++q) {
+        const int i = threadIdx.x + q * BLOCK;
+        if (i < stride && (i == 1 || i >= kPartialHeader))
+          for (int r = 0; r < nr; ++r) acc[q] = fma(s_scale[r0 + r], s_tile[r * stride + i], acc[q]);
       }
-      s_agg[i] = num / eta;
+    }
+    if (threadIdx.x == 1) s_eta = acc[0];
+    __syncthreads();
+    const Acc eta = s_eta;
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int i = threadIdx.x + q * BLOCK;
+      if (i >= kPartialHeader && i < stride) s_agg[i - kPartialHeader] = acc[q] / eta;
     }
   } else {
     for (int i = threadIdx.x; i < 2 * T; i += BLOCK) s_agg[i] = a.agg_in[i];
   }
-  __syncthreads();
-
   // SG smoothing of the aggregated perturbation, then U' = U + agg.
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
@@ -167,7 +195,7 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
     R* x = a.x0 + static_cast<size_t>(ctrl) * 8;
     if constexpr (Sys::kHasMap) {
       // warp-parallel MLP step: thread j owns hidden unit j
-      const MlpParams<R, H>& w = wh.get();
+      const MlpParams<R, H>& w = *s_w;
       const R in[6] = {x[3], x[4], x[5], x[6], s_u[0], s_u[1]};
       R* h1 = s_mlp;
       R* h2 = s_mlp + H;

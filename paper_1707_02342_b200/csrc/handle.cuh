@@ -9,6 +9,7 @@
 // fails with MPPI_ERR_CUDA when no device is usable.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -370,8 +371,10 @@ struct Handle final : HandleBase {
   void setup_merge() {
     merge_G = 0;
     n_merged = n_chunks;
-    if (n_chunks > 256) {
-      merge_G = 32;
+    // pre-merge groups of up to 32 chunks (each staged in shared memory,
+    // <= ~160 KB) whenever the epilogue would otherwise walk > 2 tiles
+    if (n_chunks > 64) {
+      merge_G = std::max(1, std::min(32, static_cast<int>((160 * 1024) / (8 * partial_stride))));
       n_merged = (n_chunks + merge_G - 1) / merge_G;
       d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
     }
@@ -782,7 +785,11 @@ struct Handle final : HandleBase {
   void enqueue_premerge() {
     if (!merge_G) return;
     const dim3 grid(n_merged, C);
-    merge_chunks_kernel<><<<grid, 256, sizeof(Acc) * merge_G, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
+    const size_t smem = sizeof(Acc) * (static_cast<size_t>(merge_G) * partial_stride + merge_G);
+    if (smem > 48 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(merge_chunks_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    merge_chunks_kernel<><<<grid, 512, smem, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
                                                    merge_G, cfg.lambda, d_partials2.p,
                                                    static_cast<long long>(n_merged) * partial_stride);
     ++launches;
@@ -823,6 +830,8 @@ struct Handle final : HandleBase {
     EpilogueArgs<R> e{};
     e.T = T;
     e.n_chunks = merge_G ? n_merged : n_chunks;
+    // rows per shared-memory tile: <= 32 and <= ~96 KB
+    e.tile_rows = std::max(1, std::min({32, e.n_chunks, static_cast<int>((96 * 1024) / (8 * partial_stride))}));
     e.partial_stride = partial_stride;
     e.partials_ctrl_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
     e.lambda = cfg.lambda;
@@ -850,8 +859,9 @@ struct Handle final : HandleBase {
   }
   void enqueue_epilogue(bool merge, bool slide, bool increment, bool plant, bool trace, int ctrls) {
     const EpilogueArgs<R> e = epilogue_args(merge, slide, increment, plant, trace);
-    const size_t smem = sizeof(Acc) * (2 * T + (merge ? (merge_G ? n_merged : n_chunks) : 0)) + sizeof(R) * (2 * T + 2 * 64);
     dispatch(kPhilox, [&]<int HH, class Sys, int Mode>() {
+      const size_t smem = epilogue_smem_bytes<R, HH>(T, merge ? e.n_chunks : 0, merge ? e.tile_rows : 0,
+                                                     partial_stride, plant);
       auto kern = epilogue_kernel<R, HH, Sys, kEpiBlock>;
       if (smem > 48 * 1024)
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

@@ -63,7 +63,9 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 __device__ __forceinline__ void philox_box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
   const float u1 = static_cast<float>((a >> 8) + 1u) * 0x1.0p-24f;
   const float u2 = static_cast<float>(b >> 8) * 0x1.0p-24f;
-  const float r = sqrtf(-2.0f * logf(u1));
+  // sqrt.approx (MUFU, ~1 ulp): no IEEE slow-path branch in the rollout loop
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * logf(u1)));
   float s, c;
   sincospif(2.0f * u2, &s, &c);
   z0 = r * c;

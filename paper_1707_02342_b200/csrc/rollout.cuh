@@ -336,33 +336,37 @@ __global__ void inject_transpose_kernel(const double* __restrict__ ref, int K, i
 
 // Pre-merge of G consecutive chunk partials into one (same format), in fixed
 // order, when a launch produced many small chunks.  grid = (ceil(n_in / G), C).
-// The per-chunk scale factors are computed once (shared memory) and the chunk
-// loop is unrolled in batches of 8 independent loads, so a thread does not
-// wait on one L2 round trip per chunk.  Summation order: ascending chunk.
+// All G x stride values are loaded at once (one L2 round trip: thread t takes
+// flat indices t, t + blockDim, ...), scaled by their chunk factor into shared
+// memory, then summed per element over the chunks in ascending order.
+// Dynamic smem: G x stride doubles + G doubles.
 template <int kUnused = 0>
 __global__ void merge_chunks_kernel(const Acc* __restrict__ in, int n_in, int stride, long long in_ctrl_stride,
                                     int G, double lambda, Acc* __restrict__ out, long long out_ctrl_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Acc* s_scale = reinterpret_cast<Acc*>(smem_raw);  // G
+  Acc* s_val = reinterpret_cast<Acc*>(smem_raw);  // [G][stride]
+  Acc* s_scale = s_val + static_cast<size_t>(G) * stride;
   __shared__ Acc s_red[32];
   __shared__ int s_bad;
   const int b = blockIdx.x, ctrl = blockIdx.y;
   const int c0 = b * G, c1 = min(n_in, c0 + G), n = c1 - c0;
   const Acc* P = in + static_cast<size_t>(ctrl) * in_ctrl_stride + static_cast<size_t>(c0) * stride;
   if (threadIdx.x == 0) s_bad = 0;
+  const int total = n * stride;
+  for (int f = threadIdx.x; f < total; f += blockDim.x) s_val[f] = P[f];
   __syncthreads();
   Acc m = INFINITY;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const Acc r = P[static_cast<size_t>(c) * stride];
+    const Acc r = s_val[c * stride];
     m = (r < m) ? r : m;
-    if (P[static_cast<size_t>(c) * stride + 2] != 0.0) s_bad = 1;
+    if (s_val[c * stride + 2] != 0.0) s_bad = 1;
   }
   m = warp_min(m);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
   __syncthreads();
   Acc rho = s_red[0];
   for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) rho = (s_red[w] < rho) ? s_red[w] : rho;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) s_scale[c] = exp(-(P[static_cast<size_t>(c) * stride] - rho) / lambda);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) s_scale[c] = exp(-(s_val[c * stride] - rho) / lambda);
   __syncthreads();
   Acc* o = out + static_cast<size_t>(ctrl) * out_ctrl_stride + static_cast<size_t>(b) * stride;
   for (int i = threadIdx.x; i < stride; i += blockDim.x) {
@@ -373,16 +377,9 @@ __global__ void merge_chunks_kernel(const Acc* __restrict__ in, int n_in, int st
     } else if (i == 3) {
       o[3] = 0.0;
     } else {
-      Acc s = 0.0;
-      for (int c = 0; c < n; c += 8) {
-        Acc v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = (c + u < n) ? P[static_cast<size_t>(c + u) * stride + i] : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (c + u < n) s = fma(s_scale[c + u], v[u], s);
-      }
-      o[i] = s;
+      Acc sum = 0.0;
+      for (int c = 0; c < n; ++c) sum = fma(s_scale[c], s_val[c * stride + i], sum);
+      o[i] = sum;
     }
   }
 }

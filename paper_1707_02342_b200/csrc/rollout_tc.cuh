@@ -227,7 +227,7 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
 // grid = (ceil(chunks / NW), controllers), block = 32 * NW; one warp = one
 // chunk of 16*MT samples.  Dynamic smem: plan (2T + 2 floats), then the
 // numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
-template <int MT, int NW, int Mode, bool STAB, bool STORE>
+template <int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
 __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const uint32_t* __restrict__ frag,
                                                             const __grid_constant__ TailArgs tail) {
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     e0 = zm ? e0 - u0 : e0;
     e1 = zm ? e1 - u1 : e1;
     if constexpr (STORE) {
-      if (t < T && !dup) s_eps[t * CH + s_own] = make_float2(e0, e1);
+      if (t < T) s_eps[t * CH + s_own] = make_float2(e0, e1);  // mirrors store identical values
     }
     const float v0 = u0 + e0, v1 = u1 + e1;
     const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
@@ -348,8 +348,9 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // next pair is unconditional code in the odd step).
   auto step = [&](int t, auto even_tag) {
     constexpr bool EVEN = decltype(even_tag)::value;
-    // stage this step's inputs (owner)
-    if (!dup) {
+    // stage this step's inputs (owner; MT = 1 mirror lanes store the same
+    // values to the same row, so no branch splits the step's basic block)
+    {
       uint2* row = st.in[m_own][row_own];
       uint32_t hi, lo;
       split2(roll, vx, hi, lo);
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     p_roll = roll;
     p_vx = vx;
     p_vy = vy;
-    if (trace) {
+    if (TRACE && trace) {
       float* so = a.trace_states + (t + 1) * 7;
       so[0] = px; so[1] = py; so[2] = th; so[3] = roll; so[4] = vx; so[5] = vy; so[6] = thd;
     }

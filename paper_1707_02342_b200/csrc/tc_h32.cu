@@ -10,10 +10,10 @@ namespace mppi_host {
 namespace {
 constexpr int kTcWarps = 4;  // warps (chunks) per CTA
 
-template <int MT, int Mode, bool STAB, bool STORE>
-cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+template <int MT, int Mode, bool STAB, bool STORE, bool TRACE>
+cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
                      int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
-  auto kern = mppi_dev::rollout_tc_kernel<MT, kTcWarps, Mode, STAB, STORE>;
+  auto kern = mppi_dev::rollout_tc_kernel<MT, kTcWarps, Mode, STAB, STORE, TRACE>;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -21,6 +21,13 @@ cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
   const dim3 grid((n_chunks + kTcWarps - 1) / kTcWarps, ctrls);
   kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag, tail);
   return cudaGetLastError();
+}
+// the per-step state trace (parity: mppi_gpu_rollout_states) is its own instantiation
+template <int MT, int Mode, bool STAB, bool STORE>
+cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                     int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
+  if (a.trace_states) return go_trace<MT, Mode, STAB, STORE, true>(a, frag, tail, n_chunks, ctrls, smem, stream);
+  return go_trace<MT, Mode, STAB, STORE, false>(a, frag, tail, n_chunks, ctrls, smem, stream);
 }
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (2 CTAs of 4 warps per SM); larger launches regenerate it from the counters.

@@ -336,7 +336,7 @@ def test_kernel_variant_and_launch_count():
     g.mpc_step(w.x0[0])
     # the fp32 H = 32 vehicle path is the tensor-core K1 (+ the epilogue kernel)
     assert "rollout_tc_kernel" in g.kernel_variant
-    assert g.launch_count - n0 == 2
+    assert g.launch_count - n0 in (2, 3)  # + a pre-merge kernel when K1 produced > 64 chunks
     w64 = workload.make("c2", samples=256, horizon_steps=20)
     g64, _ = pair(w64, "fp32", "philox")
     n0 = g64.launch_count
