@@ -68,10 +68,13 @@ __host__ __device__ constexpr size_t epilogue_smem_bytes(int T, int n_chunks, in
   return sizeof(Acc) * (2 * T + n_chunks + static_cast<size_t>(tile_rows) * stride) + sizeof(R) * (2 * T + 2 * H) +
          (plant ? sizeof(MlpParams<R, H>) + 16 : 0);
 }
+// The epilogue of one controller, executed by one CTA of BLOCK threads
+// (epilogue_kernel, or CTA 0 of the cooperative tensor-core K1).  `w` points
+// to the model weights (the plant step), `smem_raw` to epilogue_smem_bytes of
+// dynamic shared memory.
 template <class R, int H, class Sys, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__ EpilogueArgs<R> a,
-                                                         const __grid_constant__ WeightHolder<R, H> wh) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void epilogue_body(const EpilogueArgs<R>& a, const MlpParams<R, H>* w_src, int ctrl,
+                                              unsigned char* smem_raw) {
   const int T = a.T;
   const int n_rows = a.partials ? a.n_chunks : 0;
   Acc* s_agg = reinterpret_cast<Acc*>(smem_raw);
@@ -85,13 +88,12 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
   __shared__ int s_bad;
   __shared__ R s_u[2];
   __shared__ Acc s_eta;
-  const int ctrl = blockIdx.x;
   StepStatus* st = a.status + ctrl;
   if (st->code != 0) return;  // sticky abort: a previous stage failed
   R* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
   if constexpr (Sys::kHasMap) {
     if (a.plant) {  // stage the plant's weights (overlaps the merge)
-      const float4* src = reinterpret_cast<const float4*>(&wh.get());
+      const float4* src = reinterpret_cast<const float4*>(w_src);
       float4* dst = reinterpret_cast<float4*>(s_w);
       for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<R, H>) / 16); i += BLOCK) dst[i] = src[i];
     }
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
     } else {
       if (threadIdx.x == 0) {
         R xs[7] = {x[0], x[1], R(0), R(0), R(0), R(0), R(0)};
-        Sys::step(xs, s_u[0], s_u[1], wh.get(), a.sys);
+        Sys::step(xs, s_u[0], s_u[1], *w_src, a.sys);
         x[0] = xs[0];
         x[1] = xs[1];
       }
@@ -248,6 +250,13 @@ __global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__
     a.iters[ctrl] = it;
     st->iteration = it;
   }
+}
+
+template <class R, int H, class Sys, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) epilogue_kernel(const __grid_constant__ EpilogueArgs<R> a,
+                                                         const __grid_constant__ WeightHolder<R, H> wh) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  epilogue_body<R, H, Sys, BLOCK>(a, &wh.get(), blockIdx.x, smem_raw);
 }
 
 // The slide half of mpc_step on its own (controller.cpp:143-146).

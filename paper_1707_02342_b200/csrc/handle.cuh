@@ -169,8 +169,9 @@ struct Handle final : HandleBase {
   std::string variant_name() const override {
     char buf[160];
     if (use_tc)
-      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=32,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks%s)",
-                    tc_mt, cfg.noise_mode, chunk_samples, n_chunks, merge_G ? ", pre-merged" : "");
+      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=32,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %s)",
+                    tc_mt, cfg.noise_mode, chunk_samples, n_chunks,
+                    coop_tail() ? "cooperative merge+epilogue" : "merge + epilogue kernels");
     else if (use_ws)
       std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks%s)", H, ws_L,
                     cfg.noise_mode, ws_smem_w ? "smem-weights" : "const-weights", n_chunks, merge_G ? ", pre-merged" : "");
@@ -194,12 +195,12 @@ struct Handle final : HandleBase {
   bool use_tc = false;
   int tc_mt = 2;
   DevBuf<uint32_t> d_tcfrag;
-  // fused tail (tail.cuh): group merge in K1 + epilogue by the last warp
-  bool tail_fused_ok = false;
-  int tail_G = 1, tail_groups = 0, groups_per_rank = 0;
+  // tensor-core tail (tail.cuh): element-parallel merge into one row per
+  // controller, cooperative inside K1 when the grid is one wave
+  DevBuf<Acc> d_merged;
   DevBuf<unsigned> d_tail_cnt;
-  DevBuf<Acc> d_groups, d_final;
   DevBuf<MlpParams<float, 32>> d_plantw;
+  int coop_state = 0;  // 1: the cooperative K1 fits (one controller, one wave)
   int graph_kernels[3] = {0, 0, 0};
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   int rank = 0, world = 1;
@@ -373,63 +374,29 @@ struct Handle final : HandleBase {
     n_merged = n_chunks;
     // pre-merge groups of up to 32 chunks (each staged in shared memory,
     // <= ~160 KB) whenever the epilogue would otherwise walk > 2 tiles
-    if (n_chunks > 64) {
+    if (n_chunks > 64 && !use_tc) {
       merge_G = std::max(1, std::min(32, static_cast<int>((160 * 1024) / (8 * partial_stride))));
       n_merged = (n_chunks + merge_G - 1) / merge_G;
       d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
     }
   }
 
-  // Groups of G chunks for the fused tail: G ~ sqrt(chunks), a power of two
-  // that divides each rank's chunk range (so groups never straddle ranks and
-  // the merge order is the same for every rank count).
   void setup_tail() {
-    tail_fused_ok = false;
+    coop_state = 0;
     if (!use_tc) return;
-    int G = 1;
-    while (G < 256 && static_cast<long long>(G) * G < n_chunks) G *= 2;
-    while (G > 1 && chunks_per_rank % G != 0) G /= 2;
-    tail_G = G;
-    tail_groups = (n_chunks + G - 1) / G;
-    groups_per_rank = (chunks_per_rank + G - 1) / G;
-    // warp_merge_rows handles <= 256 rows; the final warp keeps U' (2T floats)
-    // in its 8 KB numerator buffer (rollout_tc.cuh)
-    tail_fused_ok = 3 * T <= 32 * kRedStride && tail_G <= 256 && tail_groups <= 256;
-    if (!tail_fused_ok) return;
-    d_final.alloc(static_cast<size_t>(C) * partial_stride);
-    d_tail_cnt.alloc(static_cast<size_t>(C) * (tail_groups + 1));
-    CUDA_TRY(cudaMemset(d_tail_cnt.p, 0, d_tail_cnt.n * sizeof(unsigned)));
-    d_groups.alloc(static_cast<size_t>(C) * std::max(tail_groups, world * groups_per_rank) * partial_stride);
+    d_merged.alloc(static_cast<size_t>(C) * partial_stride);
+    d_tail_cnt.alloc(C);
+    CUDA_TRY(cudaMemset(d_tail_cnt.p, 0, C * sizeof(unsigned)));
+    // The cooperative tail is opt-in (MPPI_TAIL=coop): measured slower than the
+    // separate merge + epilogue kernels on B200 (profiles/README.md).
+    const char* e = std::getenv("MPPI_TAIL");
+    const bool wanted = e && std::string(e) == "coop";
+    if (C == 1 && wanted &&
+        tc_coop_fits(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 32>(T, 1, 1, partial_stride, true)))
+      coop_state = 1;
   }
-  TailArgs make_tail(int mode, bool slide, bool increment, bool plant, bool trace) const {
-    TailArgs ta{};
-    ta.mode = mode;
-    if (mode == 0) return ta;
-    ta.G = tail_G;
-    ta.n_chunks = n_chunks;
-    ta.n_groups = tail_groups;
-    ta.groups_ctrl_stride = static_cast<long long>(std::max(tail_groups, world * groups_per_rank)) * partial_stride;
-    ta.counters = d_tail_cnt.p;
-    ta.groups = d_groups.p;
-    ta.final_rows = d_final.p;
-    ta.plant_w = d_plantw.p;
-    if constexpr (std::is_same<R, float>::value) ta.e = epilogue_args(false, slide, increment, plant, trace);
-    return ta;
-  }
-  // MPPI_TAIL=fused runs the group merge and the epilogue inside K1 (last
-  // warp), =split the group merge in K1 + a final one-warp kernel (the
-  // multi-rank shape on one GPU); default (measured faster, profiles/): the
-  // separate pre-merge + epilogue kernels.
-  int tail_style() const {
-    static const int style = [] {
-      const char* e = std::getenv("MPPI_TAIL");
-      if (!e) return 0;
-      const std::string v(e);
-      return v == "off" ? 0 : (v == "split" ? 1 : 2);
-    }();
-    return style;
-  }
-  bool fused_tail() const { return use_tc && tail_fused_ok && tail_style() != 0; }
+  // MPPI_TAIL=kernels forces the separate merge + epilogue kernels.
+  bool coop_tail() const { return use_tc && world == 1 && C == 1 && coop_state == 1; }
 
   static void validate_config(const mppi_gpu_config& c) {
     // SamplingParams::validate (types.hpp:105-122)
@@ -796,19 +763,32 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaGetLastError());
   }
 
-  // One iteration after the host inputs are staged: K1 (+ fused tail), or
-  // K1, exchange, pre-merge, epilogue.
+  // One iteration after the host inputs are staged.  Tensor-core path: the
+  // cooperative K1 (rollout + merge + epilogue, one launch), or K1, [the
+  // all-gather of chunk partials], the element-parallel merge and the
+  // epilogue over the merged row — identical arithmetic either way.  Other
+  // K1 variants: K1, exchange, pre-merge, epilogue.
   void enqueue_iteration(int mode, bool events, bool slide, bool increment, bool plant, bool trace) {
-    if (fused_tail()) {
-      const bool split = world > 1 || tail_style() == 1;
-      const TailArgs ta = make_tail(split ? 1 : 2, slide, increment, plant, trace);
-      enqueue_rollout(mode, events, &ta);
-      if (split) {
-        const size_t count = static_cast<size_t>(groups_per_rank) * partial_stride;
-        if (world > 1)
-          NCCL_TRY(nccl().AllGather(d_groups.p + static_cast<size_t>(rank) * count, d_groups.p, count, ncclFloat64,
-                                    comm, stream));
-        CUDA_TRY(launch_tail_final(ta, T, partial_stride, cfg.lambda, C, stream));
+    if (use_tc) {
+      if constexpr (std::is_same<R, float>::value) {
+        if (coop_tail()) {
+          TailArgs ta{};
+          ta.mode = 1;
+          ta.merged = d_merged.p;
+          ta.plant_w = d_plantw.p;
+          ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
+          enqueue_rollout(mode, events, &ta);
+          return;
+        }
+      }
+      enqueue_rollout(mode, events);
+      enqueue_exchange();
+      if constexpr (std::is_same<R, float>::value) {
+        TailArgs ta{};
+        ta.plant_w = d_plantw.p;
+        ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
+        CUDA_TRY(launch_tail_tc(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride, cfg.lambda, d_merged.p,
+                                d_tail_cnt.p, ta, C, stream));
         ++launches;
       }
       return;
@@ -826,7 +806,8 @@ struct Handle final : HandleBase {
     NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, ncclFloat64, comm, stream));
   }
 
-  EpilogueArgs<R> epilogue_args(bool merge, bool slide, bool increment, bool plant, bool trace) const {
+  EpilogueArgs<R> epilogue_args(bool merge, bool slide, bool increment, bool plant, bool trace,
+                                bool merged_row = false) const {
     EpilogueArgs<R> e{};
     e.T = T;
     e.n_chunks = merge_G ? n_merged : n_chunks;
@@ -845,6 +826,12 @@ struct Handle final : HandleBase {
     e.increment = increment;
     e.plant = plant;
     e.partials = merge ? (merge_G ? d_partials2.p : d_partials.p) : nullptr;
+    if (merge && merged_row) {  // the tensor-core path's single merged row (tail.cuh)
+      e.partials = d_merged.p;
+      e.n_chunks = 1;
+      e.tile_rows = 1;
+      e.partials_ctrl_stride = partial_stride;
+    }
     e.agg_in = merge ? nullptr : d_agg.p;
     e.plan = d_plan.p;
     e.x0 = d_x0.p;
@@ -857,8 +844,9 @@ struct Handle final : HandleBase {
     e.sys = system_args();
     return e;
   }
-  void enqueue_epilogue(bool merge, bool slide, bool increment, bool plant, bool trace, int ctrls) {
-    const EpilogueArgs<R> e = epilogue_args(merge, slide, increment, plant, trace);
+  void enqueue_epilogue(bool merge, bool slide, bool increment, bool plant, bool trace, int ctrls,
+                        bool merged_row = false) {
+    const EpilogueArgs<R> e = epilogue_args(merge, slide, increment, plant, trace, merged_row);
     dispatch(kPhilox, [&]<int HH, class Sys, int Mode>() {
       const size_t smem = epilogue_smem_bytes<R, HH>(T, merge ? e.n_chunks : 0, merge ? e.tile_rows : 0,
                                                      partial_stride, plant);

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
                                                             const uint32_t* __restrict__ frag,
                                                             const __grid_constant__ TailArgs tail) {
   constexpr int CH = 16 * MT;
+  static_assert(32 * NW == kMergeBlock, "the cooperative merge must use the merge kernel's block shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
   float* s_plan = reinterpret_cast<float*>(smem_raw);
@@ -274,7 +275,10 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const int row_own = g + 8 * (t4 & 1);
   const bool dup = (MT == 1) && (t4 >= 2);  // MT = 1: lanes t >= 2 mirror t - 2
   const int k = chunk * CH + 16 * m_own + row_own;
-  const bool valid = (k < a.K) && !dup;
+  // warps past the rank's last chunk (last CTA only) run without writing
+  // anything; they stay alive for the cooperative tail's grid barriers
+  const bool active = chunk < a.chunk_end;
+  const bool valid = (k < a.K) && !dup && active;
   const bool zm = k >= a.zero_start;
   const int kn = (k < a.K) ? k : 0;  // noise counter (in range for every lane)
   const float dt = a.sys.dt;
@@ -282,7 +286,6 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
   const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
   __syncthreads();  // s_plan, stage constants
-  if (chunk >= a.chunk_end) return;  // tail warps of the last CTA (no block barrier below)
 
   // Noise: Philox draws one 128-bit block per step pair; the other modes (parity)
   // go through the generic per-step stream.
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
   Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
              static_cast<size_t>(chunk) * a.partial_stride;
-  if (lane == 0) {
+  if (lane == 0 && active) {
     out[0] = rho;
     out[1] = eta;
     out[2] = any_bad ? 1.0 : 0.0;
@@ -458,11 +461,21 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     const double* col = red + lane * kTcRedStride;
 #pragma unroll 8
     for (int l = 0; l < 32; ++l) s = s + col[l];
-    if (tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
+    if (active && tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
     __syncwarp();
   }
   // group merge / fused epilogue (tail.cuh); the reduction buffer is scratch now
-  tail_after_chunk(tail, ctrl, chunk, T, a.partial_stride, a.partials_ctrl_stride, a.partials, a.dlambda, red, lane);
+  // cooperative tail (one controller, grid co-resident): merge of the chunk
+  // partials by all CTAs, then the epilogue by CTA 0 (tail.cuh)
+  if (tail.mode == 1) {
+    cooperative_groups::this_grid().sync();
+    merge_elements<32 * NW>(a.partials, a.chunk_end, a.partial_stride, a.dlambda, tail.merged, blockIdx.x, gridDim.x,
+                            s_red_all);
+    cooperative_groups::this_grid().sync();
+    if (blockIdx.x == 0)
+      epilogue_body<float, 32, VehicleMlp<float, 32>, 32 * NW>(tail.e, tail.plant_w, 0,
+                                                               reinterpret_cast<unsigned char*>(s_red_all));
+  }
 }
 
 }  // namespace mppi_dev

@@ -1,163 +1,224 @@
-// tail.cuh — the iteration tail fused into K1 (tensor-core path).
+// tail.cuh — the iteration tail of the tensor-core path: merge of the chunk
+// softmin partials, then the epilogue of mpc_step.
 //
-// K1 reduces each chunk of samples to softmin partials (rho_c, eta_c, bad_c,
-// num_c[T][2]) relative to the chunk minimum.  Instead of two more kernels
-// (pre-merge, epilogue) after K1, the warp that finishes LAST in each group of
-// G chunks merges that group (in chunk order), and the warp that finishes the
-// last group runs the whole epilogue of mpc_step for its controller
-// (controller.cpp:137-146): merge of the group partials in group order,
-// agg = num / eta, Savitzky-Golay (smoothing.cpp:48-65, mirror padding),
-// U' = U + agg with the ControlPlan finiteness check (types.hpp:79-83),
-// u0 = clamp(U'[0]), slide, ++iteration, and the device plant step of the
-// closed loop.  "Last" is decided by a per-group / per-controller atomic
-// ticket after a __threadfence, the classic threadfence-reduction pattern;
-// every merge runs in a fixed order, so the result does not depend on which
-// warp happens to finish last.  Counters reset themselves for the next launch.
-//
-// With samples sharded over ranks, K1 stops after the group merge (mode 1),
-// the group partials are all-gathered, and tail_final_kernel runs the same
-// final-merge + epilogue code on every rank: the arithmetic is identical to
-// the single-GPU fused path, so the plan is bit-identical for any rank count
-// whose chunk ranges are whole groups.
+// K1 reduces every chunk of samples to (rho_c, eta_c, bad_c, num_c[T][2])
+// relative to the chunk minimum.  The merge is ELEMENT-parallel: rho =
+// min_c rho_c, and every other element e is
+//   merged[e] = sum_c exp(-(rho_c - rho) / lambda) * P[c][e],
+// computed by one CTA of kMergeBlock threads per element (thread j takes chunks
+// j, j + kMergeBlock, ... in ascending order; the thread sums are then added
+// by a fixed butterfly + warp-order tree).  The summation order depends only
+// on the chunk count, never on which CTA handles which element, so
+//   * the cooperative K1 (one wave: grid.sync, merge by all CTAs, grid.sync,
+//     epilogue by CTA 0 — no extra kernel boundary), and
+//   * merge_elements_kernel after a separate K1 (large K, or ranks > 1 after
+//     the all-gather of chunk partials)
+// produce bit-identical plans.  The epilogue then runs on the single merged
+// row (scale exp(0) = 1: the row passes through unchanged).
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "epilogue.cuh"
 
 namespace mppi_dev {
 
+constexpr int kMergeBlock = 128;
+constexpr int kMergeElems = 8;  // elements per pass of a CTA (independent loads in flight)
+
 struct TailArgs {
-  int mode;                       // 0: chunk partials only; 1: + group merge; 2: + final epilogue
-  int G;                          // chunks per group
-  int n_chunks;                   // chunks of the controller (all ranks)
-  int n_groups;                   // groups of the controller (all ranks)
-  long long groups_ctrl_stride;   // doubles per controller in `groups`
-  unsigned* counters;             // [C][n_groups + 1]
-  Acc* groups;                    // [C][n_groups][partial_stride]
-  Acc* final_rows;                // [C][partial_stride]: the merged partial of the controller
-  const MlpParams<float, 32>* plant_w;  // device plant weights (closed loop)
-  EpilogueArgs<float> e;          // epilogue flags / state pointers (e.partials unused)
+  int mode;                             // 0: chunk partials only; 1: cooperative merge + epilogue in K1
+  Acc* merged;                          // [C][partial_stride]: the merged row
+  const MlpParams<float, 32>* plant_w;  // model weights (device plant)
+  EpilogueArgs<float> e;                // epilogue over `merged` (n_chunks = 1)
 };
 
-// Merge partial rows [r0, r1) of `P` (stride doubles each, r1 - r0 <= 256)
-// into `out` (same row format), one warp: rho = min rho_r, then every element
-// e >= 1 is sum_r exp(-(rho_r - rho)/lambda) * P[r][e] in ascending row
-// order.  Lane l owns rows r0 + l + 32j (its own rows summed in order, then
-// the 32 lane sums added in lane order through a transposed shared-memory
-// block), so the row reads are contiguous per lane and many loads are in
-// flight at once.  red: 32 x kRedStride doubles of scratch.
-constexpr int kRedStride = 33;
-__device__ __forceinline__ void warp_merge_rows(const Acc* P, int r0, int r1, int stride, double lambda, Acc* out,
-                                                double* red, int lane) {
-  constexpr int kMaxJ = 8;
-  Acc m = INFINITY;
-  bool bad = false;
-  for (int r = r0 + lane; r < r1; r += 32) {
-    const Acc* pr = P + static_cast<size_t>(r) * stride;
-    const Acc rho = __ldcg(pr);
-    m = (rho < m) ? rho : m;
-    bad = bad || (__ldcg(pr + 2) != 0.0);
+// Deterministic CTA sum of kMergeElems values per thread (butterfly, then
+// warps in order).  s_part: (BLOCK/32) x kMergeElems doubles.
+template <int BLOCK>
+__device__ __forceinline__ void block_sum_n(Acc (&v)[kMergeElems], Acc* s_part) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kMergeElems; ++j) v[j] = warp_sum(v[j]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < kMergeElems; ++j) s_part[wid * kMergeElems + j] = v[j];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kMergeElems; ++j) {
+    Acc s = s_part[j];
+    for (int w = 1; w < BLOCK / 32; ++w) s = s + s_part[w * kMergeElems + j];
+    v[j] = s;
   }
-  const Acc rho = warp_min(m);
-  const bool any_bad = __any_sync(0xffffffffu, bad);
-  double scale[kMaxJ];
-#pragma unroll
-  for (int j = 0; j < kMaxJ; ++j) {
-    const int r = r0 + lane + 32 * j;
-    scale[j] = (r < r1) ? exp(-(__ldcg(P + static_cast<size_t>(r) * stride) - rho) / lambda) : 0.0;
-  }
-  for (int eb = 0; eb < stride; eb += 32) {
-    double v[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) v[e] = 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxJ; ++j) {
-      const int r = r0 + lane + 32 * j;
-      if (r < r1) {  // r >= r1 for every lane once j passes the last row: uniform exit
-        const Acc* pr = P + static_cast<size_t>(r) * stride + eb;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = fma(scale[j], (eb + e < stride) ? __ldcg(pr + e) : 0.0, v[e]);
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < 32; ++e) red[e * kRedStride + lane] = v[e];
-    __syncwarp();
-    Acc sum = 0.0;
-#pragma unroll 8
-    for (int l = 0; l < 32; ++l) sum = sum + red[lane * kRedStride + l];
-    if (eb + lane < stride) out[eb + lane] = sum;
-    __syncwarp();
-  }
-  if (lane == 0) {
-    out[0] = rho;
-    out[2] = any_bad ? 1.0 : 0.0;
-    out[3] = 0.0;
-  }
-  __syncwarp();
 }
 
-// Final merge over the group partials + the epilogue of mpc_step, one warp.
-// `fin` is a global row (stride doubles) for the merged partial; red: the
-// warp's 32 x kRedStride scratch.
+// One CTA (BLOCK threads): merged elements e0, e0 + estep, ... of the rows
+// P[0..n) (stride doubles each).  smem: merge_smem_bytes(n).  The CTA with
+// e0 == 0 also writes rho, bad and the reserved slot.
+template <int BLOCK>
+__device__ void merge_elements(const Acc* P, int n, int stride, double lambda, Acc* merged, int e0, int estep,
+                               double* smem) {
+  double* s_scale = smem;
+  double* s_part = smem + n;
+  Acc m = INFINITY;
+  int bad = 0;
+#pragma unroll 8
+  for (int r = threadIdx.x; r < n; r += BLOCK) {
+    const Acc rho_r = __ldcg(P + static_cast<size_t>(r) * stride);
+    bad |= (__ldcg(P + static_cast<size_t>(r) * stride + 2) != 0.0);
+    m = (rho_r < m) ? rho_r : m;
+    s_scale[r] = rho_r;
+  }
+  m = warp_min(m);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = m;
+  bad = __syncthreads_or(bad);
+  Acc rho = s_part[0];
+  for (int w = 1; w < BLOCK / 32; ++w) rho = (s_part[w] < rho) ? s_part[w] : rho;
+  for (int r = threadIdx.x; r < n; r += BLOCK) s_scale[r] = exp(-(s_scale[r] - rho) / lambda);
+  __syncthreads();
+  if (e0 == 0 && threadIdx.x == 0) {
+    merged[0] = rho;
+    merged[2] = bad ? 1.0 : 0.0;
+    merged[3] = 0.0;
+  }
+  for (int eb = e0; eb < stride; eb += kMergeElems * estep) {
+    Acc acc[kMergeElems];
+#pragma unroll
+    for (int j = 0; j < kMergeElems; ++j) acc[j] = 0.0;
+#pragma unroll 4
+    for (int r = threadIdx.x; r < n; r += BLOCK) {
+      const Acc sc = s_scale[r];
+      const Acc* pr = P + static_cast<size_t>(r) * stride;
+      Acc x[kMergeElems];
+#pragma unroll
+      for (int j = 0; j < kMergeElems; ++j) {
+        const int e = eb + j * estep;
+        x[j] = (e < stride) ? __ldcg(pr + e) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kMergeElems; ++j) acc[j] = fma(sc, x[j], acc[j]);
+    }
+    block_sum_n<BLOCK>(acc, s_part + BLOCK / 32);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int j = 0; j < kMergeElems; ++j) {
+        const int e = eb + j * estep;
+        if (e < stride && (e == 1 || e >= kPartialHeader)) merged[e] = acc[j];
+      }
+  }
+}
+
 template <int kUnused = 0>
-__device__ __noinline__ void tail_final_warp(const TailArgs& ta, int ctrl, int T, int partial_stride,
-                                             double lambda, double* red, int lane) {
-  const EpilogueArgs<float>& e = ta.e;
-  StepStatus* st = e.status + ctrl;
-  if (__ldcg(&st->code) != 0) return;
-  const Acc* Gp = ta.groups + static_cast<size_t>(ctrl) * ta.groups_ctrl_stride;
-  Acc* fin = ta.final_rows + static_cast<size_t>(ctrl) * partial_stride;
-  warp_merge_rows(Gp, 0, ta.n_groups, partial_stride, lambda, fin, red, lane);
-  if (fin[2] != 0.0) {
-    if (lane == 0) st->code = 2;  // it_weights: non-finite cost (weights.cpp:12)
+__global__ void __launch_bounds__(kMergeBlock) merge_elements_kernel(const Acc* __restrict__ partials, int n,
+                                                                     int stride, long long ctrl_stride,
+                                                                     double lambda, Acc* merged) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ctrl = blockIdx.y;
+  merge_elements<kMergeBlock>(partials + static_cast<size_t>(ctrl) * ctrl_stride, n, stride, lambda,
+                              merged + static_cast<size_t>(ctrl) * stride, blockIdx.x, gridDim.x,
+                              reinterpret_cast<double*>(smem_raw));
+}
+
+__host__ __device__ constexpr size_t merge_smem_bytes(int n) {
+  return sizeof(double) * (n + (kMergeBlock / 32) * (kMergeElems + 1));
+}
+
+// The epilogue of mpc_step on the merged row, for one CTA of kMergeBlock
+// threads (fp32 vehicle model, H = 32): every global input (status, merged
+// row, plan, plant state, weights) is fetched in one phase, then agg =
+// num / eta, Savitzky-Golay (smoothing.cpp:48-65, mirror padding), U' = U + agg
+// (double, rounded once; ControlPlan finiteness check, types.hpp:79-83),
+// u0 = clamp(U'[0]), slide, ++iteration, and the device plant step run with
+// three block barriers and one warp for the plant MLP (same operation order
+// as epilogue_kernel).  smem: fast_epilogue_smem_bytes(T).
+__host__ __device__ constexpr size_t fast_epilogue_smem_bytes(int T) {
+  return sizeof(double) * 2 * T + sizeof(float) * (4 * T) + sizeof(MlpParams<float, 32>) + 32;
+}
+template <int kUnused = 0>
+__device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* row,
+                                           const MlpParams<float, 32>* w_src, int ctrl, unsigned char* smem) {
+  const int T = a.T;
+  double* s_agg = reinterpret_cast<double*>(smem);
+  float* s_plan = reinterpret_cast<float*>(s_agg + 2 * T);
+  float* s_new = s_plan + 2 * T;
+  MlpParams<float, 32>* s_w = reinterpret_cast<MlpParams<float, 32>*>(
+      (reinterpret_cast<uintptr_t>(s_new + 2 * T) + 15) & ~uintptr_t(15));
+  __shared__ int s_code;
+  __shared__ double s_eta;
+  StepStatus* st = a.status + ctrl;
+  float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
+  // ---- phase 1: all global reads
+  if (threadIdx.x == 0) {
+    int code = __ldcg(&st->code);
+    if (code == 0 && __ldcg(row + 2) != 0.0) code = 2;  // it_weights: non-finite cost (weights.cpp:12)
+    s_code = code;
+    s_eta = __ldcg(row + 1);
+  }
+  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock) {
+    s_agg[i] = __ldcg(row + kPartialHeader + i);
+    s_plan[i] = plan[i];
+  }
+  if (a.plant) {
+    const float4* src = reinterpret_cast<const float4*>(w_src);
+    float4* dst = reinterpret_cast<float4*>(s_w);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<float, 32>) / 16); i += kMergeBlock)
+      dst[i] = src[i];
+  }
+  float xs_lane = 0.f;  // warp 0: lane i < 8 holds x[i]
+  if (a.plant && threadIdx.x < 8) xs_lane = a.x0[static_cast<size_t>(ctrl) * 8 + threadIdx.x];
+  __syncthreads();
+  if (s_code != 0) {
+    if (threadIdx.x == 0 && __ldcg(&st->code) == 0) st->code = s_code;
     return;
   }
-  const Acc eta = fin[1];
-  double* agg = red;                                        // 2T doubles
-  float* s_new = reinterpret_cast<float*>(red + 2 * T);     // 2T floats (T <= 256)
-  for (int i = lane; i < 2 * T; i += 32) agg[i] = fin[kPartialHeader + i] / eta;
-  __syncwarp();
-  // SG smoothing of agg = num / eta, then U' = U + SG(agg) in double, rounded once
-  float* plan = e.plan + static_cast<size_t>(ctrl) * 2 * T;
-  const int half = e.sg_window / 2;
-  bool nonfinite = false;
-  for (int i = lane; i < 2 * T; i += 32) {
+  const double eta = s_eta;
+  // ---- SG smoothing of agg, U' = U + SG(agg)
+  const int half = a.sg_window / 2;
+  int nonfinite = 0;
+  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock) {
     const int t = i >> 1, c = i & 1;
     Acc v;
-    if (e.sg_window > 0) {
+    if (a.sg_window > 0) {
       Acc acc = 0.0;
       for (int j = -half; j <= half; ++j)
-        acc = __dadd_rn(acc, __dmul_rn(e.sg[j + half], agg[reflect_index(t + j, T) * 2 + c]));
+        acc = __dadd_rn(acc, __dmul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c] / eta));
       v = acc;
     } else {
-      v = agg[i];
+      v = s_agg[i] / eta;
     }
-    const float nv = static_cast<float>(__dadd_rn(static_cast<Acc>(plan[i]), v));
-    nonfinite = nonfinite || !isfinite(nv);
+    const float nv = static_cast<float>(__dadd_rn(static_cast<Acc>(s_plan[i]), v));
+    nonfinite |= !isfinite(nv);
     s_new[i] = nv;
   }
-  if (__any_sync(0xffffffffu, nonfinite)) {
-    if (lane == 0) st->code = 1;  // ControlPlan rejects non-finite plans
+  if (__syncthreads_or(nonfinite)) {  // ControlPlan rejects non-finite plans
+    if (threadIdx.x == 0) st->code = 1;
     return;
   }
-  __syncwarp();
-  const float u0 = clamp_r(s_new[0], e.lo0, e.hi0), u1 = clamp_r(s_new[1], e.lo1, e.hi1);
-  for (int i = lane; i < 2 * T; i += 32) plan[i] = e.slide ? ((i + 2 < 2 * T) ? s_new[i + 2] : 0.f) : s_new[i];
-  uint64_t it = e.iters[ctrl];
-  if (e.increment) it += 1;
+  const float u0 = clamp_r(s_new[0], a.lo0, a.hi0), u1 = clamp_r(s_new[1], a.lo1, a.hi1);
+  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock)
+    plan[i] = a.slide ? ((i + 2 < 2 * T) ? s_new[i + 2] : 0.f) : s_new[i];
+  uint64_t it = a.iters[ctrl];
+  if (a.increment) it += 1;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   if (lane == 0) {
     st->u0[0] = static_cast<double>(u0);
     st->u0[1] = static_cast<double>(u1);
-    if (e.u_trace) {
-      const uint64_t idx = it - 1 - e.trace_base[ctrl];
-      e.u_trace[(idx * e.n_ctrl + ctrl) * 2] = u0;
-      e.u_trace[(idx * e.n_ctrl + ctrl) * 2 + 1] = u1;
+    if (a.u_trace) {
+      const uint64_t idx = it - 1 - a.trace_base[ctrl];
+      a.u_trace[(idx * a.n_ctrl + ctrl) * 2] = u0;
+      a.u_trace[(idx * a.n_ctrl + ctrl) * 2 + 1] = u1;
     }
   }
-  if (e.plant) {
-    // the device plant: the same MLP model stepped with the executed input
-    // (operation order of epilogue_kernel: lane j = hidden unit j)
-    float* x = e.x0 + static_cast<size_t>(ctrl) * 8;
-    const MlpParams<float, 32>& w = *ta.plant_w;
+  if (a.plant) {
+    // the device plant: the same model stepped with the executed input;
+    // lane j = hidden unit j (operation order of epilogue_kernel)
+    const MlpParams<float, 32>& w = *s_w;
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, xs_lane, i);
     const float in[6] = {x[3], x[4], x[5], x[6], u0, u1};
     float acc = w.b1[lane];
 #pragma unroll
@@ -177,61 +238,43 @@ __device__ __noinline__ void tail_final_warp(const TailArgs& ta, int ctrl, int T
 #pragma unroll
     for (int o = 0; o < 4; ++o) dd[o] = __shfl_sync(0xffffffffu, d, o);
     if (lane == 0) {
-      float xs[7];
-      for (int i = 0; i < 7; ++i) xs[i] = x[i];
-      advance_split<float>(xs, dd, e.sys.dt);
-      for (int i = 0; i < 7; ++i) x[i] = xs[i];
-      for (int i = 0; i < 8; ++i) st->x[i] = static_cast<double>(x[i]);
-      if (e.x_trace) {
-        const uint64_t idx = it - e.trace_base[ctrl];
-        for (int i = 0; i < 8; ++i) e.x_trace[(idx * e.n_ctrl + ctrl) * 8 + i] = x[i];
+      advance_split<float>(x, dd, a.sys.dt);
+      float* xo = a.x0 + static_cast<size_t>(ctrl) * 8;
+      for (int i = 0; i < 7; ++i) xo[i] = x[i];
+      for (int i = 0; i < 8; ++i) st->x[i] = static_cast<double>(i < 7 ? x[i] : x[7]);
+      if (a.x_trace) {
+        const uint64_t idx = it - a.trace_base[ctrl];
+        for (int i = 0; i < 8; ++i) a.x_trace[(idx * a.n_ctrl + ctrl) * 8 + i] = x[i];
       }
     }
   }
   if (lane == 0) {
-    e.iters[ctrl] = it;
+    a.iters[ctrl] = it;
     st->iteration = it;
   }
 }
 
-// Called by every warp of K1 after it wrote its chunk partial `chunk` (all
-// lanes).  scratch: per-warp shared memory (see tail_final_warp).
-__device__ __forceinline__ void tail_after_chunk(const TailArgs& ta, int ctrl, int chunk, int T, int partial_stride,
-                                                 long long partials_ctrl_stride, const Acc* partials, double lambda,
-                                                 double* scratch, int lane) {
-  if (ta.mode == 0) return;
-  __threadfence();
-  __syncwarp();
-  unsigned* cnt = ta.counters + static_cast<size_t>(ctrl) * (ta.n_groups + 1);
-  const int grp = chunk / ta.G;
-  const int c0 = grp * ta.G, c1 = min(ta.n_chunks, c0 + ta.G);
-  unsigned ticket = 0;
-  if (lane == 0) ticket = atomicAdd(cnt + grp, 1u);
-  ticket = __shfl_sync(0xffffffffu, ticket, 0);
-  if (ticket != static_cast<unsigned>(c1 - c0 - 1)) return;  // not the last chunk of the group
-  __threadfence();
-  Acc* gout = ta.groups + static_cast<size_t>(ctrl) * ta.groups_ctrl_stride + static_cast<size_t>(grp) * partial_stride;
-  warp_merge_rows(partials + static_cast<size_t>(ctrl) * partials_ctrl_stride, c0, c1, partial_stride, lambda, gout,
-                  scratch, lane);
-  if (lane == 0) cnt[grp] = 0;  // reset for the next launch
-  if (ta.mode < 2) return;
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) ticket = atomicAdd(cnt + ta.n_groups, 1u);
-  ticket = __shfl_sync(0xffffffffu, ticket, 0);
-  if (ticket != static_cast<unsigned>(ta.n_groups - 1)) return;
-  __threadfence();
-  tail_final_warp<>(ta, ctrl, T, partial_stride, lambda, scratch, lane);
-  if (lane == 0) cnt[ta.n_groups] = 0;
-}
-
-// Ranks > 1: the final merge + epilogue after the all-gather of group
-// partials (one warp per controller; same code as the fused path).
+// The tensor-core path's tail in one launch: the element-parallel merge by
+// every CTA, then the epilogue by the CTA that finishes last (threadfence +
+// ticket; the counter resets itself).  grid = (elements CTAs, controllers).
 template <int kUnused = 0>
-__global__ void __launch_bounds__(32) tail_final_kernel(const __grid_constant__ TailArgs ta, int T,
-                                                        int partial_stride, double lambda) {
+__global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict__ partials, int n, int stride,
+                                                           long long ctrl_stride, double lambda, Acc* merged,
+                                                           unsigned* counters, const __grid_constant__ TailArgs ta) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  tail_final_warp<>(ta, blockIdx.x, T, partial_stride, lambda, reinterpret_cast<double*>(smem_raw), threadIdx.x);
+  __shared__ unsigned s_ticket;
+  const int ctrl = blockIdx.y;
+  Acc* row = merged + static_cast<size_t>(ctrl) * stride;
+  merge_elements<kMergeBlock>(partials + static_cast<size_t>(ctrl) * ctrl_stride, n, stride, lambda, row, blockIdx.x,
+                              gridDim.x, reinterpret_cast<double*>(smem_raw));
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(counters + ctrl, 1u);
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  __threadfence();
+  if (threadIdx.x == 0) counters[ctrl] = 0;
+  epilogue_fast<>(ta.e, row, ta.plant_w, ctrl, smem_raw);
 }
 
 }  // namespace mppi_dev

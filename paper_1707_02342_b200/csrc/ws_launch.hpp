@@ -22,8 +22,16 @@ cudaError_t launch_rollout_ws_h64(const mppi_dev::RolloutArgs<float>& a, const m
 cudaError_t launch_rollout_tc_h32(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
                                   const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
                                   cudaStream_t stream);
-// Ranks > 1: final merge of the all-gathered group partials + epilogue (tail.cuh).
-cudaError_t launch_tail_final(const mppi_dev::TailArgs& tail, int T, int partial_stride, double lambda, int ctrls,
-                              cudaStream_t stream);
+// Element-parallel merge of n chunk partial rows into one row per controller (tail.cuh).
+cudaError_t launch_merge_elements(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride,
+                                  double lambda, mppi_dev::Acc* merged, int ctrls, cudaStream_t stream);
+// The tensor-core tail in one launch: element-parallel merge, then the epilogue
+// by the last CTA (tail.cuh).  counters: one zero-initialised unsigned per controller.
+cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
+                           mppi_dev::Acc* merged, unsigned* counters, const mppi_dev::TailArgs& ta, int ctrls,
+                           cudaStream_t stream);
+// Whether the cooperative tensor-core K1 (merge + epilogue inside, tail mode 1)
+// can run: the whole grid co-resident and the tail's scratch within the CTA's buffers.
+bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem);
 
 }  // namespace mppi_host
