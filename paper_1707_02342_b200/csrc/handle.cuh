@@ -374,7 +374,9 @@ struct Handle final : HandleBase {
     n_merged = n_chunks;
     // pre-merge groups of up to 32 chunks (each staged in shared memory,
     // <= ~160 KB) whenever the epilogue would otherwise walk > 2 tiles
-    if (n_chunks > 64 && !use_tc) {
+    // (tensor-core path: its element-parallel tail stages one scale per row in
+    // shared memory, so only very large launches pre-merge)
+    if ((!use_tc && n_chunks > 64) || (use_tc && n_chunks > 8192)) {
       merge_G = std::max(1, std::min(32, static_cast<int>((160 * 1024) / (8 * partial_stride))));
       n_merged = (n_chunks + merge_G - 1) / merge_G;
       d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
@@ -787,8 +789,12 @@ struct Handle final : HandleBase {
         TailArgs ta{};
         ta.plant_w = d_plantw.p;
         ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
-        CUDA_TRY(launch_tail_tc(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride, cfg.lambda, d_merged.p,
-                                d_tail_cnt.p, ta, C, stream));
+        enqueue_premerge();
+        const Acc* rows = merge_G ? d_partials2.p : d_partials.p;
+        const int n_rows = merge_G ? n_merged : n_chunks;
+        const long long rows_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
+        CUDA_TRY(launch_tail_tc(rows, n_rows, partial_stride, rows_stride, cfg.lambda, d_merged.p, d_tail_cnt.p, ta, C,
+                                stream));
         ++launches;
       }
       return;

@@ -162,10 +162,13 @@ constexpr int kTcTB = 16;  // timesteps per block of the numerator reduction
 constexpr int kTcRedStride = 33;  // doubles per row (padding: conflict-free column reads)
 
 // MLP of one step for MT tiles: inputs from the stage, outputs d3 (fp32).
-template <int MT>
+// side1 / side2: independent per-sample work of the step, placed between the
+// layers so the scheduler interleaves it with the tensor-core chains (it
+// otherwise lands after the MLP as a separate dependent block).
+template <int MT, class Side1, class Side2>
 __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, const uint32_t (&w1)[8],
                                        const uint32_t (&w2)[32], const uint32_t (&w3)[8], const float (&b2)[8],
-                                       const float (&b3)[2], float (&d3)[MT][4]) {
+                                       const float (&b3)[2], float (&d3)[MT][4], Side1&& side1, Side2&& side2) {
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     // ---- layer 1 (k8): A rows g, g+8; k = 2t, 2t+1 (bias through the constant-one column)
@@ -181,6 +184,7 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
       mma_k8(a.m, ag.x, ag8.x, w1[2 * j]);      // hi * hi
       acc2_sum(a, d1[j]);
     }
+    if (m == MT - 1) side1();
     // ---- layer 2 (2 x k16)
     Acc2 a2[4];
 #pragma unroll
@@ -205,6 +209,7 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
     float d2[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc2_sum(a2[j], d2[j]);
+    if (m == MT - 1) side2();
     // ---- layer 3 (2 x k16, n = 8: outputs 0..3)
     Acc2 a3;
     a3.m[0] = a3.m[2] = b3[0];
@@ -365,16 +370,16 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     }
     __syncwarp();
     float d3[MT][4];
-    tc_mlp<MT>(st, g, t4, w1, w2, w3, b2, b3, d3);
     // independent of this step's MLP (overlaps it): running cost of step t-1
     // on x_t (taps fetched last step), and v_{t+1}
-    {
-      const float h = map_interp(q);
-      const float rc = tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[t > 0 ? t - 1 : 0], cp);
-      cost += (t > 0) ? static_cast<Acc>(add_rn(rc, p_coup)) : 0.0;
-    }
-    p_coup = coup_t;
-    produce_v(t + 1, !EVEN);
+    tc_mlp<MT>(st, g, t4, w1, w2, w3, b2, b3, d3,
+               [&] {
+                 const float h = map_interp(q);
+                 const float rc = tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[t > 0 ? t - 1 : 0], cp);
+                 cost += (t > 0) ? static_cast<Acc>(add_rn(rc, p_coup)) : 0.0;
+                 p_coup = coup_t;
+               },
+               [&] { produce_v(t + 1, !EVEN); });
     // outputs to their owners: columns 2t, 2t+1 live in lanes t = 0, 1
     if (t4 < 2) {
 #pragma unroll
