@@ -74,9 +74,9 @@ constexpr int kBlock = 128;      // samples per chunk / K1 CTA
 // Per-lane mma.sync fragment table of the tensor-core rollout
 // (rollout_tc.cuh, word map there): weights folded with the tanh identity
 // tanh(z) = 1 - 2 / (1 + 2^(kz)), k = 2 log2 e, then split hi/lo in fp16.
-template <class R>
-std::vector<uint32_t> tc_build_fragments(const MlpParams<R, 32>& w) {
-  constexpr int H = 32;
+template <class R, int H>
+std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
+  using L = mppi_dev::TcLayout<H>;
   const double kk2 = 2.0 / std::log(2.0);
   auto W1 = [&](int n, int i) { return static_cast<double>(w.w1t[i][n]); };
   auto W2 = [&](int n, int i) { return static_cast<double>(w.w2t[i][n]); };
@@ -96,27 +96,28 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, 32>& w) {
   auto pack = [&](double lo_k, double hi_k, int which) -> uint32_t {
     return static_cast<uint32_t>(hl(lo_k, which)) | (static_cast<uint32_t>(hl(hi_k, which)) << 16);
   };
-  std::vector<uint32_t> f(static_cast<size_t>(mppi_dev::kTcWords) * 32, 0u);
+  std::vector<uint32_t> f(static_cast<size_t>(L::WORDS) * 32, 0u);
   auto put = [&](int word, int lane, uint32_t v) { f[static_cast<size_t>(word) * 32 + lane] = v; };
   for (int lane = 0; lane < 32; ++lane) {
     const int g = lane >> 2, t = lane & 3;
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < L::NJ; ++j)
       for (int which = 0; which < 2; ++which)
-        put(2 * j + which, lane, pack(B1(2 * t, 8 * j + g), B1(2 * t + 1, 8 * j + g), which));
-    for (int kk = 0; kk < 2; ++kk)
-      for (int j = 0; j < 4; ++j)
+        put(L::W1 + 2 * j + which, lane, pack(B1(2 * t, 8 * j + g), B1(2 * t + 1, 8 * j + g), which));
+    for (int kk = 0; kk < L::NK; ++kk)
+      for (int j = 0; j < L::NJ; ++j)
         for (int r = 0; r < 2; ++r)
           for (int which = 0; which < 2; ++which) {
             const int i0 = 16 * kk + 2 * t + 8 * r;
-            put(8 + ((kk * 4 + j) * 2 + r) * 2 + which, lane, pack(B2(i0, 8 * j + g), B2(i0 + 1, 8 * j + g), which));
+            put(L::W2 + ((kk * L::NJ + j) * 2 + r) * 2 + which, lane,
+                pack(B2(i0, 8 * j + g), B2(i0 + 1, 8 * j + g), which));
           }
-    for (int kk = 0; kk < 2; ++kk)
+    for (int kk = 0; kk < L::NK; ++kk)
       for (int r = 0; r < 2; ++r)
         for (int which = 0; which < 2; ++which) {
           const int i0 = 16 * kk + 2 * t + 8 * r;
-          put(40 + (kk * 2 + r) * 2 + which, lane, pack(B3(i0, g), B3(i0 + 1, g), which));
+          put(L::W3 + (kk * 2 + r) * 2 + which, lane, pack(B3(i0, g), B3(i0 + 1, g), which));
         }
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < L::NJ; ++j)
       for (int c = 0; c < 2; ++c) {
         const int n = 8 * j + 2 * t + c;
         double sum = 0.0;
@@ -124,7 +125,7 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, 32>& w) {
         const float v = static_cast<float>(kk2 * (static_cast<double>(w.b2[n]) + sum));
         uint32_t bits;
         std::memcpy(&bits, &v, 4);
-        put(48 + 2 * j + c, lane, bits);
+        put(L::B2 + 2 * j + c, lane, bits);
       }
     for (int c = 0; c < 2; ++c) {
       const int n = 2 * t + c;
@@ -136,7 +137,7 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, 32>& w) {
       }
       uint32_t bits;
       std::memcpy(&bits, &v, 4);
-      put(56 + c, lane, bits);
+      put(L::B3 + c, lane, bits);
     }
   }
   return f;
@@ -169,8 +170,8 @@ struct Handle final : HandleBase {
   std::string variant_name() const override {
     char buf[160];
     if (use_tc)
-      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=32,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %s)",
-                    tc_mt, cfg.noise_mode, chunk_samples, n_chunks,
+      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=%d,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %s)",
+                    H, tc_mt, cfg.noise_mode, chunk_samples, n_chunks,
                     coop_tail() ? "cooperative merge+epilogue" : "merge + epilogue kernels");
     else if (use_ws)
       std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks%s)", H, ws_L,
@@ -199,7 +200,7 @@ struct Handle final : HandleBase {
   // controller, cooperative inside K1 when the grid is one wave
   DevBuf<Acc> d_merged;
   DevBuf<unsigned> d_tail_cnt;
-  DevBuf<MlpParams<float, 32>> d_plantw;
+  DevBuf<unsigned char> d_plantw;  // MlpParams<float, H> (the plant step of the tail)
   int coop_state = 0;  // 1: the cooperative K1 fits (one controller, one wave)
   int graph_kernels[3] = {0, 0, 0};
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
@@ -339,10 +340,11 @@ struct Handle final : HandleBase {
     const bool f32_vehicle = std::is_same<R, float>::value && cfg.system == MPPI_SYSTEM_VEHICLE_MLP;
     // default K1 for the fp32 vehicle model: tensor cores at H = 32, FFMA2
     // warp-specialised at H = 64 (its weights do not fit the register file)
-    use_tc = f32_vehicle && H == 32 && !force_generic && kernel != "ws";
+    use_tc = f32_vehicle && !force_generic && kernel != "ws";
     if (use_tc) {
       tc_mt = K <= 32768 ? 1 : 2;  // one m16 tile per warp while warps are scarce
-      if (const char* mv = std::getenv("MPPI_TC_MT")) tc_mt = std::atoi(mv) == 1 ? 1 : 2;
+      if (H == 64) tc_mt = 1;     // (the H = 64 kernel keeps one tile per warp)
+      if (const char* mv = std::getenv("MPPI_TC_MT"); mv && H == 32) tc_mt = std::atoi(mv) == 1 ? 1 : 2;
       chunk_samples = 16 * tc_mt;
       return;
     }
@@ -394,7 +396,8 @@ struct Handle final : HandleBase {
     const char* e = std::getenv("MPPI_TAIL");
     const bool wanted = e && std::string(e) == "coop";
     if (C == 1 && wanted &&
-        tc_coop_fits(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 32>(T, 1, 1, partial_stride, true)))
+        (H == 32 ? tc_coop_fits<32>(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 32>(T, 1, 1, partial_stride, true))
+                 : tc_coop_fits<64>(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 64>(T, 1, 1, partial_stride, true))))
       coop_state = 1;
   }
   // MPPI_TAIL=kernels forces the separate merge + epilogue kernels.
@@ -471,19 +474,20 @@ struct Handle final : HandleBase {
     };
     for (int i = 0; i < H * 6; ++i)
       if (!std::isfinite(w1[i])) throw_invalid("MLP weights must be finite");
+    auto upload_tc = [&](const auto& w) {
+      if (!use_tc) return;
+      std::vector<uint32_t> frag = tc_build_fragments(w);
+      d_tcfrag.alloc(frag.size());
+      CUDA_TRY(cudaMemcpy(d_tcfrag.p, frag.data(), frag.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+      d_plantw.alloc(sizeof(w));
+      CUDA_TRY(cudaMemcpy(d_plantw.p, &w, sizeof(w), cudaMemcpyHostToDevice));
+    };
     if (H == 32) {
       fill(*w32);
-      if (use_tc) {
-        std::vector<uint32_t> frag = tc_build_fragments(*w32);
-        d_tcfrag.alloc(frag.size());
-        CUDA_TRY(cudaMemcpy(d_tcfrag.p, frag.data(), frag.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-        if constexpr (std::is_same<R, float>::value) {
-          d_plantw.alloc(1);
-          CUDA_TRY(cudaMemcpy(d_plantw.p, w32.get(), sizeof(MlpParams<float, 32>), cudaMemcpyHostToDevice));
-        }
-      }
+      upload_tc(*w32);
     } else {
       fill(*w64);
+      upload_tc(*w64);
       if (!kWeightsByValue<R, 64>) {
         d_w64.alloc(1);
         CUDA_TRY(cudaMemcpy(d_w64.p, w64.get(), sizeof(MlpParams<R, 64>), cudaMemcpyHostToDevice));
@@ -726,8 +730,8 @@ struct Handle final : HandleBase {
     else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
     if (use_tc) {
       if constexpr (std::is_same<R, float>::value)
-        CUDA_TRY(launch_rollout_tc_h32(a, d_tcfrag.p, tail ? *tail : no_tail, mode, tc_mt, chunk_hi - chunk_lo, C,
-                                       stream));
+        CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(
+            a, d_tcfrag.p, tail ? *tail : no_tail, mode, tc_mt, chunk_hi - chunk_lo, C, stream));
     } else if (use_ws) {
       launch_ws(a, mode, grid);
     } else {
@@ -793,8 +797,8 @@ struct Handle final : HandleBase {
         const Acc* rows = merge_G ? d_partials2.p : d_partials.p;
         const int n_rows = merge_G ? n_merged : n_chunks;
         const long long rows_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
-        CUDA_TRY(launch_tail_tc(rows, n_rows, partial_stride, rows_stride, cfg.lambda, d_merged.p, d_tail_cnt.p, ta, C,
-                                stream));
+        CUDA_TRY((H == 32 ? launch_tail_tc<32> : launch_tail_tc<64>)(rows, n_rows, partial_stride, rows_stride,
+                                                                      cfg.lambda, d_merged.p, d_tail_cnt.p, ta, C, stream));
         ++launches;
       }
       return;
@@ -1175,8 +1179,8 @@ struct Handle final : HandleBase {
       CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
       if (use_tc) {
         if constexpr (std::is_same<R, float>::value)
-          CUDA_TRY(launch_rollout_tc_h32(a, d_tcfrag.p, TailArgs{}, effective_mode(batch_injected), tc_mt, n_chunks,
-                                         1, stream));
+          CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(
+              a, d_tcfrag.p, TailArgs{}, effective_mode(batch_injected), tc_mt, n_chunks, 1, stream));
       } else {
         launch_ws(a, effective_mode(batch_injected), dim3(n_chunks, 1));
       }

@@ -39,13 +39,23 @@
 
 namespace mppi_dev {
 
-// Per-lane fragment words, stored [word][lane] (coalesced load at kernel start).
-//   0..7    B1 (k8 x n8) n-tile j: hi = 2j, lo = 2j+1
-//   8..39   B2 (k16 x n8): 8 + ((kk*4 + j)*2 + r)*2 + hl    (r: b0/b1)
-//   40..47  B3 (k16 x n8, outputs 0..3): 40 + (kk*2 + r)*2 + hl
-//   48..55  bias2 (fp32 bits): 48 + j*2 + c, column 8j + 2t + c
-//   56..57  bias3 (fp32 bits): column 2t + c (zero for t >= 2)
-constexpr int kTcWords = 58;
+// Per-lane fragment words, stored [word][lane] (coalesced load at kernel start),
+// for H hidden units (NJ = H/8 output n-tiles, NK = H/16 input k-tiles):
+//   W1 .. : B1 (k8 x n8) n-tile j: hi = 2j, lo = 2j+1
+//   W2 .. : B2 (k16 x n8): W2 + ((kk*NJ + j)*2 + r)*2 + hl    (r: b0/b1)
+//   W3 .. : B3 (k16 x n8, outputs 0..3): W3 + (kk*2 + r)*2 + hl
+//   B2 .. : bias2 (fp32 bits): B2 + j*2 + c, column 8j + 2t + c
+//   B3 .. : bias3 (fp32 bits): column 2t + c (zero for t >= 2)
+// H = 32 keeps every fragment in registers; at H = 64 the 128 layer-2 words
+// live in shared memory (one LDS.128 per (kk, j), shared by the CTA's warps).
+template <int H>
+struct TcLayout {
+  static constexpr int NJ = H / 8, NK = H / 16;
+  static constexpr int W1 = 0, W2 = 2 * NJ, W3 = W2 + 4 * NK * NJ, B2 = W3 + 4 * NK, B3 = B2 + 2 * NJ;
+  static constexpr int WORDS = B3 + 2;
+  static constexpr bool W2_SMEM = H > 32;
+};
+constexpr int kTcWords = TcLayout<32>::WORDS;  // 58
 constexpr int kTcH = 32;
 
 __device__ __forceinline__ void mma_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
@@ -164,18 +174,21 @@ constexpr int kTcRedStride = 33;  // doubles per row (padding: conflict-free col
 // MLP of one step for MT tiles: inputs from the stage, outputs d3 (fp32).
 // side1 / side2: independent per-sample work of the step, placed between the
 // layers so the scheduler interleaves it with the tensor-core chains (it
-// otherwise lands after the MLP as a separate dependent block).
-template <int MT, class Side1, class Side2>
-__device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, const uint32_t (&w1)[8],
-                                       const uint32_t (&w2)[32], const uint32_t (&w3)[8], const float (&b2)[8],
-                                       const float (&b3)[2], float (&d3)[MT][4], Side1&& side1, Side2&& side2) {
+// otherwise lands after the MLP as a separate dependent block).  b2frag(kk, j)
+// returns the layer-2 B fragment words (b0 hi, b0 lo, b1 hi, b1 lo).
+template <int H, int MT, class B2Frag, class Side1, class Side2>
+__device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, const uint32_t (&w1)[2 * (H / 8)],
+                                       B2Frag&& b2frag, const uint32_t (&w3)[4 * (H / 16)],
+                                       const float (&b2)[2 * (H / 8)], const float (&b3)[2], float (&d3)[MT][4],
+                                       Side1&& side1, Side2&& side2) {
+  constexpr int NJ = H / 8, NK = H / 16;
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     // ---- layer 1 (k8): A rows g, g+8; k = 2t, 2t+1 (bias through the constant-one column)
     const uint2 ag = st.in[m][g][t4], ag8 = st.in[m][g + 8][t4];
-    float d1[4][4];
+    float d1[NJ][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       Acc2 a;
 #pragma unroll
       for (int i = 0; i < 4; ++i) a.m[i] = a.c[i] = 0.f;
@@ -185,39 +198,39 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
       acc2_sum(a, d1[j]);
     }
     if (m == MT - 1) side1();
-    // ---- layer 2 (2 x k16)
-    Acc2 a2[4];
+    // ---- layer 2 (NK x k16)
+    Acc2 a2[NJ];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       a2[j].m[0] = a2[j].m[2] = b2[2 * j];
       a2[j].m[1] = a2[j].m[3] = b2[2 * j + 1];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a2[j].c[i] = 0.f;
     }
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
+    for (int kk = 0; kk < NK; ++kk) {
       uint32_t ahi[4], alo[4];
       acc_to_a(d1[2 * kk], d1[2 * kk + 1], ahi, alo);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int b = (kk * 4 + j) * 4;  // b0 hi, b0 lo, b1 hi, b1 lo
-        mma_k16(a2[j].c, alo, w2[b], w2[b + 2]);
-        mma_k16(a2[j].c, ahi, w2[b + 1], w2[b + 3]);
-        mma_k16(a2[j].m, ahi, w2[b], w2[b + 2]);
+      for (int j = 0; j < NJ; ++j) {
+        const uint4 b = b2frag(kk, j);  // b0 hi, b0 lo, b1 hi, b1 lo
+        mma_k16(a2[j].c, alo, b.x, b.z);
+        mma_k16(a2[j].c, ahi, b.y, b.w);
+        mma_k16(a2[j].m, ahi, b.x, b.z);
       }
     }
-    float d2[4][4];
+    float d2[NJ][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc2_sum(a2[j], d2[j]);
+    for (int j = 0; j < NJ; ++j) acc2_sum(a2[j], d2[j]);
     if (m == MT - 1) side2();
-    // ---- layer 3 (2 x k16, n = 8: outputs 0..3)
+    // ---- layer 3 (NK x k16, n = 8: outputs 0..3)
     Acc2 a3;
     a3.m[0] = a3.m[2] = b3[0];
     a3.m[1] = a3.m[3] = b3[1];
 #pragma unroll
     for (int i = 0; i < 4; ++i) a3.c[i] = 0.f;
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
+    for (int kk = 0; kk < NK; ++kk) {
       uint32_t ahi[4], alo[4];
       acc_to_a(d2[2 * kk], d2[2 * kk + 1], ahi, alo);
       const int b = kk * 4;
@@ -232,7 +245,7 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
 // grid = (ceil(chunks / NW), controllers), block = 32 * NW; one warp = one
 // chunk of 16*MT samples.  Dynamic smem: plan (2T + 2 floats), then the
 // numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
-template <int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
+template <int H, int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
 __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const uint32_t* __restrict__ frag,
                                                             const __grid_constant__ TailArgs tail) {
@@ -257,19 +270,37 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   for (int i = threadIdx.x; i < 2 * T + 2; i += 32 * NW)
     s_plan[i] = (i < 2 * T) ? a.plan[static_cast<size_t>(ctrl) * 2 * T + i] : 0.f;
 
-  // weights + biases into registers (loop-invariant for the whole rollout)
-  uint32_t w1[8], w2[32], w3[8];
-  float b2[8], b3[2];
+  // weights + biases into registers (loop-invariant for the whole rollout);
+  // at H = 64 the layer-2 fragments go to shared memory instead
+  using L = TcLayout<H>;
+  uint32_t w1[2 * L::NJ], w3[4 * L::NK];
+  uint32_t w2r[L::W2_SMEM ? 1 : 4 * L::NK * L::NJ];
+  float b2[2 * L::NJ], b3[2];
+  __shared__ __align__(16) uint4 s_w2[L::W2_SMEM ? L::NK * L::NJ : 1][32];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w1[i] = frag[i * 32 + lane];
+  for (int i = 0; i < 2 * L::NJ; ++i) w1[i] = frag[(L::W1 + i) * 32 + lane];
+  if constexpr (L::W2_SMEM) {
+    for (int f = warp; f < L::NK * L::NJ; f += NW)
+      s_w2[f][lane] = make_uint4(frag[(L::W2 + 4 * f) * 32 + lane], frag[(L::W2 + 4 * f + 1) * 32 + lane],
+                                 frag[(L::W2 + 4 * f + 2) * 32 + lane], frag[(L::W2 + 4 * f + 3) * 32 + lane]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) w2[i] = frag[(8 + i) * 32 + lane];
+    for (int i = 0; i < 4 * L::NK * L::NJ; ++i) w2r[i] = frag[(L::W2 + i) * 32 + lane];
+  }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) w3[i] = frag[(40 + i) * 32 + lane];
+  for (int i = 0; i < 4 * L::NK; ++i) w3[i] = frag[(L::W3 + i) * 32 + lane];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) b2[i] = __uint_as_float(frag[(48 + i) * 32 + lane]);
-  b3[0] = __uint_as_float(frag[56 * 32 + lane]);
-  b3[1] = __uint_as_float(frag[57 * 32 + lane]);
+  for (int i = 0; i < 2 * L::NJ; ++i) b2[i] = __uint_as_float(frag[(L::B2 + i) * 32 + lane]);
+  b3[0] = __uint_as_float(frag[L::B3 * 32 + lane]);
+  b3[1] = __uint_as_float(frag[(L::B3 + 1) * 32 + lane]);
+  auto b2frag = [&](int kk, int j) -> uint4 {
+    if constexpr (L::W2_SMEM) {
+      return s_w2[kk * L::NJ + j][lane];
+    } else {
+      const int b = (kk * L::NJ + j) * 4;
+      return make_uint4(w2r[b], w2r[b + 1], w2r[b + 2], w2r[b + 3]);
+    }
+  };
 
   TcStage<MT>& st = s_stage[warp];
   // the constant-one input column (k = 6: bias of layer 1), written once
@@ -372,7 +403,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     float d3[MT][4];
     // independent of this step's MLP (overlaps it): running cost of step t-1
     // on x_t (taps fetched last step), and v_{t+1}
-    tc_mlp<MT>(st, g, t4, w1, w2, w3, b2, b3, d3,
+    tc_mlp<H, MT>(st, g, t4, w1, b2frag, w3, b2, b3, d3,
                [&] {
                  const float h = map_interp(q);
                  const float rc = tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[t > 0 ? t - 1 : 0], cp);
@@ -478,8 +509,8 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
                             s_red_all);
     cooperative_groups::this_grid().sync();
     if (blockIdx.x == 0)
-      epilogue_body<float, 32, VehicleMlp<float, 32>, 32 * NW>(tail.e, tail.plant_w, 0,
-                                                               reinterpret_cast<unsigned char*>(s_red_all));
+      epilogue_body<float, H, VehicleMlp<float, H>, 32 * NW>(
+          tail.e, static_cast<const MlpParams<float, H>*>(tail.plant_w), 0, reinterpret_cast<unsigned char*>(s_red_all));
   }
 }
 

@@ -29,7 +29,7 @@ constexpr int kMergeElems = 8;  // elements per pass of a CTA (independent loads
 struct TailArgs {
   int mode;                             // 0: chunk partials only; 1: cooperative merge + epilogue in K1
   Acc* merged;                          // [C][partial_stride]: the merged row
-  const MlpParams<float, 32>* plant_w;  // model weights (device plant)
+  const void* plant_w;                  // MlpParams<float, H> of the model (device plant)
   EpilogueArgs<float> e;                // epilogue over `merged` (n_chunks = 1)
 };
 
@@ -126,24 +126,27 @@ __host__ __device__ constexpr size_t merge_smem_bytes(int n) {
 }
 
 // The epilogue of mpc_step on the merged row, for one CTA of kMergeBlock
-// threads (fp32 vehicle model, H = 32): every global input (status, merged
-// row, plan, plant state, weights) is fetched in one phase, then agg =
-// num / eta, Savitzky-Golay (smoothing.cpp:48-65, mirror padding), U' = U + agg
-// (double, rounded once; ControlPlan finiteness check, types.hpp:79-83),
-// u0 = clamp(U'[0]), slide, ++iteration, and the device plant step run with
-// three block barriers and one warp for the plant MLP (same operation order
-// as epilogue_kernel).  smem: fast_epilogue_smem_bytes(T).
+// threads (fp32 vehicle model, H = 32 or 64): every global input (status,
+// merged row, plan, plant state, weights) is fetched in one phase, then
+// agg = num / eta, Savitzky-Golay (smoothing.cpp:48-65, mirror padding),
+// U' = U + agg (double, rounded once; ControlPlan finiteness check,
+// types.hpp:79-83), u0 = clamp(U'[0]), slide, ++iteration, and the device
+// plant step run with three block barriers and one warp for the plant MLP
+// (lane j owns hidden units j, j + 32, ...; the operation order of each unit
+// is that of epilogue_kernel).  smem: fast_epilogue_smem_bytes<H>(T).
+template <int H>
 __host__ __device__ constexpr size_t fast_epilogue_smem_bytes(int T) {
-  return sizeof(double) * 2 * T + sizeof(float) * (4 * T) + sizeof(MlpParams<float, 32>) + 32;
+  return sizeof(double) * 2 * T + sizeof(float) * (4 * T) + sizeof(MlpParams<float, H>) + 32;
 }
-template <int kUnused = 0>
+template <int H>
 __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* row,
-                                           const MlpParams<float, 32>* w_src, int ctrl, unsigned char* smem) {
+                                           const MlpParams<float, H>* w_src, int ctrl, unsigned char* smem) {
+  constexpr int U = H / 32;  // hidden units per lane
   const int T = a.T;
   double* s_agg = reinterpret_cast<double*>(smem);
   float* s_plan = reinterpret_cast<float*>(s_agg + 2 * T);
   float* s_new = s_plan + 2 * T;
-  MlpParams<float, 32>* s_w = reinterpret_cast<MlpParams<float, 32>*>(
+  MlpParams<float, H>* s_w = reinterpret_cast<MlpParams<float, H>*>(
       (reinterpret_cast<uintptr_t>(s_new + 2 * T) + 15) & ~uintptr_t(15));
   __shared__ int s_code;
   __shared__ double s_eta;
@@ -163,7 +166,7 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
   if (a.plant) {
     const float4* src = reinterpret_cast<const float4*>(w_src);
     float4* dst = reinterpret_cast<float4*>(s_w);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<float, 32>) / 16); i += kMergeBlock)
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<float, H>) / 16); i += kMergeBlock)
       dst[i] = src[i];
   }
   float xs_lane = 0.f;  // warp 0: lane i < 8 holds x[i]
@@ -213,27 +216,38 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     }
   }
   if (a.plant) {
-    // the device plant: the same model stepped with the executed input;
-    // lane j = hidden unit j (operation order of epilogue_kernel)
-    const MlpParams<float, 32>& w = *s_w;
+    const MlpParams<float, H>& w = *s_w;
     float x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, xs_lane, i);
     const float in[6] = {x[3], x[4], x[5], x[6], u0, u1};
-    float acc = w.b1[lane];
+    float h1[U], h2[U];
 #pragma unroll
-    for (int i = 0; i < 6; ++i) acc = fma_r(w.w1t[i][lane], in[i], acc);
-    const float h1 = tanh_r(acc);
-    acc = w.b2[lane];
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) acc = fma_r(w.w2t[i][lane], __shfl_sync(0xffffffffu, h1, i), acc);
-    const float h2 = tanh_r(acc);
-    float d = (lane < 4) ? w.b3[lane] : 0.f;
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const float hi = __shfl_sync(0xffffffffu, h2, i);
-      if (lane < 4) d = fma_r(w.w3t[i][lane], hi, d);
+    for (int u = 0; u < U; ++u) {
+      const int j = lane + 32 * u;
+      float acc = w.b1[j];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) acc = fma_r(w.w1t[i][j], in[i], acc);
+      h1[u] = tanh_r(acc);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = lane + 32 * u;
+      float acc = w.b2[j];
+#pragma unroll
+      for (int uu = 0; uu < U; ++uu)
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) acc = fma_r(w.w2t[32 * uu + i][j], __shfl_sync(0xffffffffu, h1[uu], i), acc);
+      h2[u] = tanh_r(acc);
+    }
+    float d = (lane < 4) ? w.b3[lane] : 0.f;
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu)
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const float hi = __shfl_sync(0xffffffffu, h2[uu], i);
+        if (lane < 4) d = fma_r(w.w3t[32 * uu + i][lane], hi, d);
+      }
     float dd[4];
 #pragma unroll
     for (int o = 0; o < 4; ++o) dd[o] = __shfl_sync(0xffffffffu, d, o);
@@ -241,7 +255,7 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
       advance_split<float>(x, dd, a.sys.dt);
       float* xo = a.x0 + static_cast<size_t>(ctrl) * 8;
       for (int i = 0; i < 7; ++i) xo[i] = x[i];
-      for (int i = 0; i < 8; ++i) st->x[i] = static_cast<double>(i < 7 ? x[i] : x[7]);
+      for (int i = 0; i < 8; ++i) st->x[i] = static_cast<double>(x[i]);
       if (a.x_trace) {
         const uint64_t idx = it - a.trace_base[ctrl];
         for (int i = 0; i < 8; ++i) a.x_trace[(idx * a.n_ctrl + ctrl) * 8 + i] = x[i];
@@ -257,7 +271,7 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
 // The tensor-core path's tail in one launch: the element-parallel merge by
 // every CTA, then the epilogue by the CTA that finishes last (threadfence +
 // ticket; the counter resets itself).  grid = (elements CTAs, controllers).
-template <int kUnused = 0>
+template <int H>
 __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict__ partials, int n, int stride,
                                                            long long ctrl_stride, double lambda, Acc* merged,
                                                            unsigned* counters, const __grid_constant__ TailArgs ta) {
@@ -274,7 +288,7 @@ __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
   if (threadIdx.x == 0) counters[ctrl] = 0;
-  epilogue_fast<>(ta.e, row, ta.plant_w, ctrl, smem_raw);
+  epilogue_fast<H>(ta.e, row, static_cast<const MlpParams<float, H>*>(ta.plant_w), ctrl, smem_raw);
 }
 
 }  // namespace mppi_dev

@@ -1,0 +1,164 @@
+// tc_launch.cuh — launchers of the tensor-core rollout kernel (rollout_tc.cuh)
+// and its tail, templated on the hidden width H; instantiated once per H by
+// tc_h32.cu / tc_h64.cu (define TC_H before including) so the variants build
+// in parallel.
+#include "rollout_tc.cuh"
+#include "ws_launch.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace mppi_host {
+
+namespace {
+constexpr int kTcWarps = 4;  // warps (chunks) per CTA
+
+template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE>
+cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                     int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
+  auto kern = mppi_dev::rollout_tc_kernel<H, MT, kTcWarps, Mode, STAB, STORE, TRACE>;
+  // (static + dynamic shared memory may pass 48 KB even when `smem` does not:
+  // the H = 64 kernel holds its layer-2 fragments in 16 KB of static smem)
+  {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid((n_chunks + kTcWarps - 1) / kTcWarps, ctrls);
+  if (tail.mode == 1) {  // cooperative: the tail's grid barriers need the whole grid co-resident
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(32 * kTcWarps);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, frag, tail);
+  }
+  kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag, tail);
+  return cudaGetLastError();
+}
+// the per-step state trace (parity: mppi_gpu_rollout_states) is its own instantiation
+template <int H, int MT, int Mode, bool STAB, bool STORE>
+cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                     int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
+  if (a.trace_states) return go_trace<H, MT, Mode, STAB, STORE, true>(a, frag, tail, n_chunks, ctrls, smem, stream);
+  return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, tail, n_chunks, ctrls, smem, stream);
+}
+// eps' stays on chip when the grid still fits one wave with that footprint
+// (2 CTAs of 4 warps per SM); larger launches regenerate it from the counters.
+template <int H, int MT, int Mode, bool STAB>
+cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+               int n_chunks, int ctrls, cudaStream_t stream) {
+  const size_t plan_bytes = (sizeof(float) * (2 * a.T + 2) + 15) & ~size_t(15);
+  const size_t base = plan_bytes + sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
+  // (the cooperative tail reuses the numerator buffers; tc_coop_fits checks they suffice)
+  const size_t eps_bytes = sizeof(float2) * kTcWarps * a.T * 16 * MT;
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const long long ctas = static_cast<long long>((n_chunks + kTcWarps - 1) / kTcWarps) * ctrls;
+  const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
+                                                   : (base + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
+  if (store) return go_store<H, MT, Mode, STAB, true>(a, frag, tail, n_chunks, ctrls, base + eps_bytes, stream);
+  return go_store<H, MT, Mode, STAB, false>(a, frag, tail, n_chunks, ctrls, base, stream);
+}
+template <int H, int Mode, bool STAB>
+cudaError_t by_mt(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail, int mt,
+                  int n_chunks, int ctrls, cudaStream_t stream) {
+  if constexpr (H > 32) {  // one m16 tile per warp (register budget of the H = 64 accumulators)
+    return go<H, 1, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream);
+  } else {
+    return mt == 1 ? go<H, 1, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream)
+                   : go<H, 2, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream);
+  }
+}
+template <int H, int Mode>
+cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                    int mt, int n_chunks, int ctrls, cudaStream_t stream) {
+  // the side-slip term (atan) is compiled in only when its weight is nonzero
+  return a.sys.cost.alpha_stab != 0.f ? by_mt<H, Mode, true>(a, frag, tail, mt, n_chunks, ctrls, stream)
+                                      : by_mt<H, Mode, false>(a, frag, tail, mt, n_chunks, ctrls, stream);
+}
+}  // namespace
+
+template <int H>
+cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
+                              const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
+                              cudaStream_t stream) {
+  switch (mode) {
+    case mppi_dev::kInjected: return by_stab<H, mppi_dev::kInjected>(a, frag, tail, mt, n_chunks, ctrls, stream);
+    case mppi_dev::kRefSplitmix: return by_stab<H, mppi_dev::kRefSplitmix>(a, frag, tail, mt, n_chunks, ctrls, stream);
+    default: return by_stab<H, mppi_dev::kPhilox>(a, frag, tail, mt, n_chunks, ctrls, stream);
+  }
+}
+
+template <int H>
+cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
+                           mppi_dev::Acc* merged, unsigned* counters, const mppi_dev::TailArgs& ta, int ctrls,
+                           cudaStream_t stream) {
+  const size_t smem = std::max(mppi_dev::merge_smem_bytes(n), mppi_dev::fast_epilogue_smem_bytes<H>(ta.e.T));
+  auto kern = mppi_dev::tail_kernel<H>;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid(std::min(stride, 296), ctrls);
+  kern<<<grid, mppi_dev::kMergeBlock, smem, stream>>>(partials, n, stride, ctrl_stride, lambda, merged, counters, ta);
+  return cudaGetLastError();
+}
+
+template <int H>
+bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem) {
+  // the tail works in the CTA's numerator buffers
+  const size_t red = sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
+  if (mppi_dev::merge_smem_bytes(n_chunks) > red || epilogue_smem > red) return false;
+  const size_t plan_bytes = (sizeof(float) * (2 * T + 2) + 15) & ~size_t(15);
+  const size_t eps_bytes = sizeof(float2) * kTcWarps * T * 16 * mt;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long ctas = (n_chunks + kTcWarps - 1) / kTcWarps;
+  // the launcher's own choice of the on-chip eps' variant (go() above)
+  const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
+                                                   : (plan_bytes + red + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
+  const size_t smem = plan_bytes + red + (store ? eps_bytes : 0);
+  int per_sm = 0;
+  auto occ = [&](auto kern) {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kTcWarps, smem);
+    return r;
+  };
+  using mppi_dev::rollout_tc_kernel;
+  using mppi_dev::kPhilox;
+  cudaError_t e;
+  if constexpr (H > 32) {
+    e = store ? occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, true, false>)
+              : occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, false, false>);
+  } else {
+    if (mt == 1)
+      e = store ? occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, true, false>)
+                : occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, false, false>);
+    else
+      e = store ? occ(rollout_tc_kernel<H, 2, kTcWarps, kPhilox, false, true, false>)
+                : occ(rollout_tc_kernel<H, 2, kTcWarps, kPhilox, false, false, false>);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return ctas <= static_cast<long long>(per_sm) * sms;
+}
+
+template cudaError_t launch_rollout_tc<TC_H>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
+                                             const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
+template cudaError_t launch_tail_tc<TC_H>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*, unsigned*,
+                                          const mppi_dev::TailArgs&, int, cudaStream_t);
+template bool tc_coop_fits<TC_H>(int, int, int, size_t);
+
+}  // namespace mppi_host

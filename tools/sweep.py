@@ -11,9 +11,12 @@ sys.path.insert(0, ROOT)
 
 
 def run(cfg, K, variant, L, steps=30, sw=1):
-    for v in ("MPPI_KERNEL", "MPPI_WS_L", "MPPI_WS_SMEM_W", "MPPI_TC_MT"):
-        os.environ.pop(v, None)
-    if variant == "generic":
+    if variant != "env":  # "env": keep the caller's MPPI_* selection
+        for v in ("MPPI_KERNEL", "MPPI_WS_L", "MPPI_WS_SMEM_W", "MPPI_TC_MT"):
+            os.environ.pop(v, None)
+    if variant == "env":
+        pass
+    elif variant == "generic":
         os.environ["MPPI_KERNEL"] = "generic"
     elif variant == "tc":
         if L:
@@ -59,7 +62,7 @@ if __name__ == "__main__":
         for cfg, K, env in json.loads(sys.argv[2]):
             e = dict(os.environ)
             e.update(env)
-            r = subprocess.run([sys.executable, __file__, "one", cfg, str(K), "tc", "0"], capture_output=True,
+            r = subprocess.run([sys.executable, __file__, "one", cfg, str(K), "env", "0"], capture_output=True,
                                text=True, env=e)
             print(json.dumps(env), r.stdout.strip() or r.stderr[-500:], flush=True)
         sys.exit(0)
