@@ -9,8 +9,7 @@
 #include <cstdlib>
 
 namespace mppi_host {
-
-namespace {
+namespace tc_detail {
 constexpr int kTcWarps = 4;  // warps (chunks) per CTA
 
 template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE>
@@ -44,7 +43,10 @@ cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
 template <int H, int MT, int Mode, bool STAB, bool STORE>
 cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
                      int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
-  if (a.trace_states) return go_trace<H, MT, Mode, STAB, STORE, true>(a, frag, tail, n_chunks, ctrls, smem, stream);
+  // (a trace is a parity call: no on-chip eps' variant is compiled for it)
+  if constexpr (!STORE) {
+    if (a.trace_states) return go_trace<H, MT, Mode, STAB, false, true>(a, frag, tail, n_chunks, ctrls, smem, stream);
+  }
   return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, tail, n_chunks, ctrls, smem, stream);
 }
 // eps' stays on chip when the grid still fits one wave with that footprint
@@ -65,7 +67,11 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, cons
   const long long ctas = static_cast<long long>((n_chunks + kTcWarps - 1) / kTcWarps) * ctrls;
   const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
                                                    : (base + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
-  if (store) return go_store<H, MT, Mode, STAB, true>(a, frag, tail, n_chunks, ctrls, base + eps_bytes, stream);
+  // (MT = 2 serves K > 32768, whose grid never fits one wave: no on-chip eps')
+  if constexpr (MT == 1) {
+    if (store && !a.trace_states)
+      return go_store<H, MT, Mode, STAB, true>(a, frag, tail, n_chunks, ctrls, base + eps_bytes, stream);
+  }
   return go_store<H, MT, Mode, STAB, false>(a, frag, tail, n_chunks, ctrls, base, stream);
 }
 template <int H, int Mode, bool STAB>
@@ -85,18 +91,7 @@ cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
   return a.sys.cost.alpha_stab != 0.f ? by_mt<H, Mode, true>(a, frag, tail, mt, n_chunks, ctrls, stream)
                                       : by_mt<H, Mode, false>(a, frag, tail, mt, n_chunks, ctrls, stream);
 }
-}  // namespace
-
-template <int H>
-cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
-                              const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
-                              cudaStream_t stream) {
-  switch (mode) {
-    case mppi_dev::kInjected: return by_stab<H, mppi_dev::kInjected>(a, frag, tail, mt, n_chunks, ctrls, stream);
-    case mppi_dev::kRefSplitmix: return by_stab<H, mppi_dev::kRefSplitmix>(a, frag, tail, mt, n_chunks, ctrls, stream);
-    default: return by_stab<H, mppi_dev::kPhilox>(a, frag, tail, mt, n_chunks, ctrls, stream);
-  }
-}
+}  // namespace tc_detail
 
 template <int H>
 cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
@@ -115,6 +110,7 @@ cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, lon
 
 template <int H>
 bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem) {
+  using tc_detail::kTcWarps;
   // the tail works in the CTA's numerator buffers
   const size_t red = sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
   if (mppi_dev::merge_smem_bytes(n_chunks) > red || epilogue_smem > red) return false;
@@ -155,10 +151,14 @@ bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem) {
   return ctas <= static_cast<long long>(per_sm) * sms;
 }
 
-template cudaError_t launch_rollout_tc<TC_H>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                             const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
+#ifdef TC_MODE
+template cudaError_t tc_detail::by_stab<TC_H, TC_MODE>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
+                                                        const mppi_dev::TailArgs&, int, int, int, cudaStream_t);
+#endif
+#ifdef TC_TAIL
 template cudaError_t launch_tail_tc<TC_H>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*, unsigned*,
                                           const mppi_dev::TailArgs&, int, cudaStream_t);
 template bool tc_coop_fits<TC_H>(int, int, int, size_t);
+#endif
 
 }  // namespace mppi_host

@@ -17,6 +17,13 @@ cudaError_t launch_rollout_ws_h32(const mppi_dev::RolloutArgs<float>& a, const m
 cudaError_t launch_rollout_ws_h64(const mppi_dev::RolloutArgs<float>& a, const mppi_dev::WeightHolder<float, 64>& w,
                                   int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
 
+namespace tc_detail {
+// the per-(H, noise mode) launchers, one translation unit each (tc_h*_*.cu)
+template <int H, int Mode>
+cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
+                    int mt, int n_chunks, int ctrls, cudaStream_t stream);
+}  // namespace tc_detail
+
 // Tensor-core rollout (rollout_tc.cuh) for hidden width H (32, 64): `frag` is
 // the per-lane fragment table built by tc_build_fragments; n_chunks chunks of
 // 16*mt samples from a.chunk0 (mt is 1 at H = 64).
@@ -34,10 +41,6 @@ cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, lon
 // can run: the whole grid co-resident and the tail's scratch within the CTA's buffers.
 template <int H>
 bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem);
-extern template cudaError_t launch_rollout_tc<32>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                                  const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
-extern template cudaError_t launch_rollout_tc<64>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                                  const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
 extern template cudaError_t launch_tail_tc<32>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*,
                                                unsigned*, const mppi_dev::TailArgs&, int, cudaStream_t);
 extern template cudaError_t launch_tail_tc<64>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*,
