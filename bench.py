@@ -160,7 +160,7 @@ def run_reference(args):
     cb = reference_cpu(w, steps, warm, sample_k)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
             "warmup": warm, "ms_per_step": cb["ms_per_step"] * (w.params.samples / sample_k),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config}: K={w.params.samples}, T={w.params.horizon_steps}, H={w.hidden}",
                        "parallelism": f"{cb['cores']} CPU threads"},
@@ -194,16 +194,22 @@ def run_ours(args):
         pg = dist
 
     w = workload.make(args.config, samples=args.samples)
+    fleet = w.controllers > 1
+    # fleet (c3): the independent controllers are split over the ranks, no
+    # communicator; otherwise the samples of one controller are sharded
+    C = max(1, w.controllers // world) if fleet else 1
     ctrl = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox",
-                      device=local, n_controllers=1)
+                      device=local, n_controllers=C)
     ctrl.set_mlp(w.mlp)
     ctrl.set_costmap(w.costmap)
-    if world > 1:
+    if fleet:
+        ctrl.perturb_fleet_costmaps(0.02, workload.SEED + rank)  # per-controller N(0, 0.02^2) map noise
+    elif world > 1:
         obj = [Controller.nccl_unique_id() if rank == 0 else None]
         pg.broadcast_object_list(obj, src=0)
         ctrl.set_comm(rank, world, obj[0])
     K, T = w.params.samples, w.params.horizon_steps
-    x0 = w.x0[0]
+    x0 = w.x0[rank * C:(rank + 1) * C] if fleet else w.x0[0]
     stream = torch.cuda.ExternalStream(ctrl.stream)
 
     def barrier():
@@ -227,33 +233,35 @@ def run_ours(args):
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
     ms_max, k1_avg_ms = float(t[0]), float(t[1])
     ms_per_step = ms_max / args.steps
-    value = K * T * args.steps / (ms_max * 1e-3)  # all ranks together process K samples per iteration
+    units_per_step = (C * world if fleet else 1) * K * T  # sample-steps of the whole job per iteration
+    value = units_per_step * args.steps / (ms_max * 1e-3)
 
     # end to end through the public API: host x0 -> H2D, step, D2H u0, every step
     e2e = None
     if not args.no_e2e:
-        x = x0.copy()
+        x = np.array(x0, dtype=np.float64).reshape(C, 7)
         for _ in range(3):
             ctrl.mpc_step(x)
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
-            u = ctrl.mpc_step(x)
+            u = np.asarray(ctrl.mpc_step(x)).reshape(C, 2)
             # host plant (outside the controller): kinematic pose update, the
             # executed throttle nudges v_x
-            x[0] += (np.cos(x[2]) * x[4] - np.sin(x[2]) * x[5]) * w.params.dt
-            x[1] += (np.sin(x[2]) * x[4] + np.cos(x[2]) * x[5]) * w.params.dt
-            x[2] += x[6] * w.params.dt
-            x[4] += 0.5 * u[1] * w.params.dt
+            px, py, th, vx, vy = x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy(), x[:, 4].copy(), x[:, 5].copy()
+            x[:, 0] = px + (np.cos(th) * vx - np.sin(th) * vy) * w.params.dt
+            x[:, 1] = py + (np.sin(th) * vx + np.cos(th) * vy) * w.params.dt
+            x[:, 2] = th + x[:, 6] * w.params.dt
+            x[:, 4] = vx + 0.5 * u[:, 1] * w.params.dt
         ev1.record(stream)
         ev1.synchronize()
         e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
         if pg:
             pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
         e_ms = float(e_ms[0])
-        e2e = {"value": K * T * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
-               "h2d_bytes_per_step": 8 * 4, "d2h_bytes_per_step": 96,
+        e2e = {"value": units_per_step * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
+               "h2d_bytes_per_step": C * 8 * 4, "d2h_bytes_per_step": C * 96,
                "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H"}
 
     if rank != 0:
@@ -262,22 +270,27 @@ def run_ours(args):
         return
 
     flop_unit = workload.flops_per_sample_step(w.hidden)
-    k_local = K // world if world > 1 else K
+    k_local = K * C if fleet else (K // world if world > 1 else K)
     k1_flops = k_local * T * flop_unit
     peak, clk = fp32_peak_tflops(local)
     achieved = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else None
     traffic, traffic_src = load_traffic()
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not fleet:
         cb = reference_cpu(w, steps=3, warmup=1, sample_k=min(K, 2048))
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        # the total work (K samples of one controller, or the 512-controller
+        # fleet) is fixed and split over the GPUs
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Xavier MLP, 2000x2000 ellipse map, Philox noise)",
         "config": {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, H={w.hidden}, MLP vehicle, "
-                               f"receding horizon with device plant",
-                   "samples": K, "horizon": T, "hidden": w.hidden, "parallelism": f"samples sharded over {world} GPU(s)",
+                               f"receding horizon with device plant"
+                               + (f", fleet of {C * world} controllers (perturbed maps)" if fleet else ""),
+                   "samples": K, "horizon": T, "hidden": w.hidden, "controllers": C * world,
+                   "parallelism": (f"{C} independent controllers per GPU on {world} GPU(s), no communication"
+                                   if fleet else f"samples sharded over {world} GPU(s)"),
                    "l2": "flushed between timed iterations (256 MiB memset, excluded from timing)",
                    "kernel": ctrl.kernel_variant},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

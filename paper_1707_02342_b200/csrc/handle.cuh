@@ -342,7 +342,9 @@ struct Handle final : HandleBase {
     // warp-specialised at H = 64 (its weights do not fit the register file)
     use_tc = f32_vehicle && !force_generic && kernel != "ws";
     if (use_tc) {
-      tc_mt = K <= 32768 ? 1 : 2;  // one m16 tile per warp while warps are scarce
+      // one m16 tile per warp while warps are scarce (counting every
+      // controller of a fleet), two once the grid fills the GPU several times
+      tc_mt = static_cast<long long>(K) * C <= 32768 ? 1 : 2;
       if (H == 64) tc_mt = 1;     // (the H = 64 kernel keeps one tile per warp)
       if (const char* mv = std::getenv("MPPI_TC_MT"); mv && H == 32) tc_mt = std::atoi(mv) == 1 ? 1 : 2;
       chunk_samples = 16 * tc_mt;
@@ -644,6 +646,8 @@ struct Handle final : HandleBase {
     a.seeds = d_seeds.p;
     a.iters = d_iters.p;
     a.abort_flag = reinterpret_cast<const int*>(d_status.p);  // StepStatus.code is the first field
+    static_assert(sizeof(StepStatus) % sizeof(int) == 0, "StepStatus must be a whole number of ints");
+    a.abort_stride = static_cast<int>(sizeof(StepStatus) / sizeof(int));
     a.costs = d_costs.p;
     a.partials = d_partials.p;
     return a;

@@ -48,7 +48,8 @@ struct RolloutArgs {
   const R* inj;           // injected batch, device layout [T][K][2]
   const uint64_t* seeds;  // [C]
   const uint64_t* iters;  // [C]
-  const int* abort_flag;  // [C] sticky status codes: nonzero -> skip
+  const int* abort_flag;  // sticky status code of controller c at abort_flag[c * abort_stride]: nonzero -> skip
+  int abort_stride;       // ints between consecutive controllers' codes (sizeof(StepStatus) / 4)
   Acc* costs;             // [C][K]
   Acc* partials;          // [C][chunks][partial_stride]
   R* trace_states;        // (T+1) x 7 trajectory of sample trace_k (or nullptr)
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ 
   R* s_plan = reinterpret_cast<R*>(s_num + (BLOCK / 32) * 2 * a.T);
   __shared__ Acc s_red[BLOCK / 32];
   const int ctrl = blockIdx.y;
-  if (a.abort_flag[ctrl] != 0) return;
+  if (a.abort_flag[static_cast<size_t>(ctrl) * a.abort_stride] != 0) return;
   const int chunk = a.chunk0 + blockIdx.x;
   const int k = chunk * BLOCK + threadIdx.x;
   const bool valid = k < a.K;

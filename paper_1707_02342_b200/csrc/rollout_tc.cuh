@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   __shared__ __align__(16) TcStage<MT> s_stage[NW];
 
   const int ctrl = blockIdx.y;
-  if (a.abort_flag[ctrl] != 0) return;
+  if (a.abort_flag[static_cast<size_t>(ctrl) * a.abort_stride] != 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int chunk = a.chunk0 + blockIdx.x * NW + warp;

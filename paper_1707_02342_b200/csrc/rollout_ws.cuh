@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(32 * L, 1) rollout_ws_kernel(const __grid_cons
   __shared__ __align__(16) WsSmem<H, L> sm;
 
   const int ctrl = blockIdx.y;
-  if (a.abort_flag[ctrl] != 0) return;
+  if (a.abort_flag[static_cast<size_t>(ctrl) * a.abort_stride] != 0) return;
   const int role = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int chunk = a.chunk0 + blockIdx.x;

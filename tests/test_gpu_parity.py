@@ -283,6 +283,22 @@ def test_fleet_controllers_are_independent():
             us = s.mpc_step(w.x0[c])
         assert np.array_equal(us, ug[c])
         assert np.array_equal(s.plan, g.get_plan(c))
+    # the receding-horizon loop on the device (sticky per-controller status
+    # across iterations): every fleet member equals its own single-controller
+    # loop, on the fp64 generic path and on the fp32 tensor-core path
+    for prec in ("fp64", "fp32"):
+        g = Controller(w.params, w.bounds, w.sg, w.cost, precision=prec, noise="philox", n_controllers=3)
+        g.set_mlp(w.mlp)
+        g.set_costmap(w.costmap)
+        ug, xg = g.closed_loop(w.x0, 6)
+        for c in range(3):
+            s = Controller(w.params, w.bounds, w.sg, w.cost, precision=prec, noise="philox")
+            s.set_mlp(w.mlp)
+            s.set_costmap(w.costmap)
+            s.set_seed(w.params.seed + c)
+            us, xs = s.closed_loop(w.x0[c], 6)
+            assert np.array_equal(us[:, 0], ug[:, c]), (prec, c)
+            assert np.array_equal(xs[:, 0], xg[:, c]), (prec, c)
     # per-controller perturbed maps change the costs but keep the loop finite
     f = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox", n_controllers=3)
     f.set_mlp(w.mlp)
