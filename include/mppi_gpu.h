@@ -73,8 +73,12 @@ enum { MPPI_FP32 = 0, MPPI_FP64 = 1 };
  * RolloutSystem).  VEHICLE_MLP = make_vehicle_system over MlpModel
  * (controller.cpp:7-35, dynamics.cpp:197-210); QUADRATIC = the reference test
  * fixture quadratic_system (test_controller.cpp:23-37): x' = x + v dt,
- * running cost quad_cost_scale * |x|^2, terminal 0, no clamping. */
-enum { MPPI_SYSTEM_VEHICLE_MLP = 0, MPPI_SYSTEM_QUADRATIC = 1 };
+ * running cost quad_cost_scale * |x|^2, terminal 0, no clamping.
+ * VEHICLE_BASIS = make_vehicle_system over BasisFunctionModel
+ * (dynamics.hpp:151-162): the 25 basis functions of eval_basis
+ * (dynamics.cpp:83-133) times the 25 x 4 Theta (step_basis_model,
+ * dynamics.cpp:152-157), with the same costs as VEHICLE_MLP. */
+enum { MPPI_SYSTEM_VEHICLE_MLP = 0, MPPI_SYSTEM_QUADRATIC = 1, MPPI_SYSTEM_VEHICLE_BASIS = 2 };
 
 /* Weight rule (controller.hpp:32). Only IT is implemented on the device. */
 enum { MPPI_WEIGHT_IT = 0, MPPI_WEIGHT_CEM = 1 };
@@ -154,6 +158,10 @@ int mppi_gpu_destroy(mppi_gpu_handle* h);
 int mppi_gpu_set_dynamics_mlp(mppi_gpu_handle* h, int hidden, const double* w1,
                               const double* b1, const double* w2, const double* b2,
                               const double* w3, const double* b3);
+/* BasisFunctionModel Theta (dynamics.hpp:75-82): theta[b*4 + o] = coeffs(b, o),
+ * b < 25 basis functions, o < 4 outputs (roll_dot, vx_dot, vy_dot,
+ * theta_ddot) — the row order of save_theta / load_theta (dynamics.cpp:230-254). */
+int mppi_gpu_set_dynamics_basis(mppi_gpu_handle* h, const double* theta);
 /* CostMap (costs.hpp:11-38); validated like CostMap::validate.  controller < 0
  * sets the map shared by every controller of the handle. */
 int mppi_gpu_set_costmap(mppi_gpu_handle* h, int controller, const double* values,

@@ -254,6 +254,59 @@ void advance_split(const R x[7], const R d[4], R dt, R n[7]) {
   n[6] = x[6] + d[3] * dt;
 }
 
+// ----------------------------------------------- basis-function model ------
+// eval_basis (dynamics.cpp:83-133); kSlipGuardSpeed = 0.1 (dynamics.cpp:47).
+template <class R>
+void eval_basis(R roll, R v_x, R v_y, R r, R u_delta, R u_F, R phi[25]) {
+  R alpha_f, alpha_r, ratio;
+  if (v_x > R(0.1)) {
+    ratio = v_y / v_x;
+    alpha_f = std::atan(ratio + R(0.45) * r / v_x - u_delta);
+    alpha_r = std::atan(ratio - R(0.35) * r / v_x);
+  } else {
+    ratio = R(0);
+    alpha_f = -u_delta;
+    alpha_r = R(0);
+  }
+  const R tf = std::tan(alpha_f), tr = std::tan(alpha_r), sd = std::sin(u_delta);
+  phi[0] = u_F;
+  phi[1] = v_x / R(10.0);
+  phi[2] = sd * tf / R(1200.0);
+  phi[3] = sd * tf * std::abs(tf) / R(1200.0 * 1200.0);
+  phi[4] = sd * tf * tf * tf / R(1200.0 * 1200.0 * 1200.0);
+  phi[5] = r * v_y / R(25.0);
+  phi[6] = r / R(10.0);
+  phi[7] = v_y / R(10.0);
+  phi[8] = sd;
+  phi[9] = ratio / R(40.0);
+  phi[10] = tf / R(1400.0);
+  phi[11] = tf * std::abs(tf) / R(1400.0 * 1400.0);
+  phi[12] = tf * tf * tf / R(1400.0 * 1400.0 * 1400.0);
+  phi[13] = tr / R(40.0);
+  phi[14] = tr * std::abs(tr) / R(40.0 * 40.0);
+  phi[15] = tr * tr * tr / R(40.0 * 40.0 * 40.0);
+  phi[16] = r * v_x / R(50.0);
+  phi[17] = roll;
+  phi[18] = roll * r;
+  phi[19] = roll * v_x / R(3.0);
+  phi[20] = roll * v_x * r / R(5.0);
+  phi[21] = v_x * v_x / R(100.0);
+  phi[22] = v_x * v_x * v_x / R(1000.0);
+  phi[23] = u_F * u_F;
+  phi[24] = u_F * u_F * u_F;
+}
+// step_basis_model (dynamics.cpp:152-157): xd_dot = coeffs^T phi, the sum over
+// the 25 basis functions in ascending order (Eigen's GEMV order is not
+// reproduced), then advance_split.
+template <class R>
+void basis_dot(const R theta[100], const R phi[25], R d[4]) {
+  for (int o = 0; o < 4; ++o) {
+    R acc = theta[o] * phi[0];
+    for (int b = 1; b < 25; ++b) acc = acc + theta[b * 4 + o] * phi[b];
+    d[o] = acc;
+  }
+}
+
 // CostMap (costs.hpp:11-38)
 template <class R>
 struct Map {
@@ -346,6 +399,31 @@ System<R> make_vehicle_system(const Mlp<R>& mlp, const R lo[2], const R hi[2],
     const R in[6] = {x[3], x[4], x[5], x[6], clampv(v[0], l0, h0), clampv(v[1], l1, h1)};
     R d[4];
     mlp_forward(in, mlp, d);          // step_mlp_model (dynamics.cpp:206-210)
+    advance_split(x, d, dt, xn);
+  };
+  s.running_cost = [&map, &cp](const R* x, int t) { return state_cost(x, t, map, cp); };
+  if (with_terminal) {
+    s.terminal_cost = [&map, &cp, horizon](const R* x) { return state_cost(x, horizon, map, cp); };
+  } else {
+    s.terminal_cost = [](const R*) { return R(0); };
+  }
+  return s;
+}
+
+// make_vehicle_system (controller.cpp:7-35) over a BasisFunctionModel
+// (dynamics.hpp:151-162).
+template <class R>
+System<R> make_basis_system(const std::vector<R>& theta, const R lo[2], const R hi[2], const Map<R>& map,
+                            const Cost<R>& cp, R dt, int horizon, bool with_terminal) {
+  if (!(dt > R(0))) throw std::invalid_argument("step_basis_model: dt must be > 0");
+  System<R> s;
+  s.state_dim = 7;
+  s.control_dim = 2;
+  const R l0 = lo[0], l1 = lo[1], h0 = hi[0], h1 = hi[1];
+  s.step = [&theta, l0, l1, h0, h1, dt](const R* x, const R* v, int, R* xn) {
+    R phi[25], d[4];
+    eval_basis<R>(x[3], x[4], x[5], x[6], clampv(v[0], l0, h0), clampv(v[1], l1, h1), phi);
+    basis_dot<R>(theta.data(), phi, d);
     advance_split(x, d, dt, xn);
   };
   s.running_cost = [&map, &cp](const R* x, int t) { return state_cost(x, t, map, cp); };
@@ -514,6 +592,7 @@ struct Controller {
   Cost<R> cost;
   std::vector<R> injected;   // reference layout, INJECTED mode
   Batch<R> last_batch;       // batch of the last rollout (post-mutation)
+  std::vector<R> theta;  // basis-function model coeffs, theta[b*4 + o]
   bool has_mlp = false, has_map = false;
 
   int T() const { return p.horizon_steps; }
@@ -521,8 +600,11 @@ struct Controller {
   System<R> system() const {
     if (cfg.system == MPPI_SYSTEM_QUADRATIC)
       return make_quadratic_system<R>(2, static_cast<R>(p.dt), static_cast<R>(cfg.quad_cost_scale));
-    if (!has_mlp) throw std::invalid_argument("vehicle system: MLP weights not set");
+    if (!has_mlp) throw std::invalid_argument("vehicle system: model (MLP weights / basis Theta) not set");
     if (!has_map) throw std::invalid_argument("vehicle system: costmap not set");
+    if (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS)
+      return make_basis_system<R>(theta, lo, hi, map, cost, static_cast<R>(p.dt), p.horizon_steps,
+                                  cfg.with_terminal != 0);
     return make_vehicle_system<R>(mlp, lo, hi, map, cost, static_cast<R>(p.dt), p.horizon_steps,
                                   cfg.with_terminal != 0);
   }
@@ -880,6 +962,32 @@ int oracle_set_mlp(AnyController* h, int H, const double* w1, const double* b1, 
     (void)sizeof(R);
     c.has_mlp = true;
   });
+}
+int oracle_set_theta(AnyController* h, const double* theta) {
+  return orc::dispatch(h, [&](auto& c) {
+    using R = typename std::decay_t<decltype(c.plan)>::value_type;
+    c.theta.resize(100);
+    for (int i = 0; i < 100; ++i) {
+      if (!std::isfinite(theta[i])) throw std::invalid_argument("load_theta: non-finite entry");
+      c.theta[i] = static_cast<R>(theta[i]);
+    }
+    c.has_mlp = true;
+  });
+}
+// eval_basis (dynamics.cpp:83-133) in double: x_d = (roll, v_x, v_y, r), v = (steer, throttle).
+int oracle_eval_basis(const double x_d[4], const double v[2], double phi[25]) {
+  orc::eval_basis<double>(x_d[0], x_d[1], x_d[2], x_d[3], v[0], v[1], phi);
+  return 0;
+}
+// step_basis_model (dynamics.cpp:152-157) in double (no clamp: the reference
+// step takes the already-clamped input).
+int oracle_step_basis(const double x[7], const double v[2], double dt, const double theta[100], double out[7]) {
+  if (!(dt > 0.0)) return 1;
+  double phi[25], d[4];
+  orc::eval_basis<double>(x[3], x[4], x[5], x[6], v[0], v[1], phi);
+  orc::basis_dot<double>(theta, phi, d);
+  orc::advance_split<double>(x, d, dt, out);
+  return 0;
 }
 int oracle_set_costmap(AnyController* h, const double* values, int W, int H, double x0,
                        double y0, double res) {

@@ -25,7 +25,7 @@ MPPI_ERR_UNSUPPORTED = 6
 
 NOISE_INJECTED, NOISE_REF_SPLITMIX, NOISE_PHILOX = 0, 1, 2
 FP32, FP64 = 0, 1
-SYSTEM_VEHICLE_MLP, SYSTEM_QUADRATIC = 0, 1
+SYSTEM_VEHICLE_MLP, SYSTEM_QUADRATIC, SYSTEM_VEHICLE_BASIS = 0, 1, 2
 WEIGHT_IT, WEIGHT_CEM = 0, 1
 
 
@@ -112,6 +112,7 @@ _SIGNATURES = {
     "mppi_gpu_create": (c_int, [_P(ConfigC), _P(c_void_p)]),
     "mppi_gpu_destroy": (c_int, [c_void_p]),
     "mppi_gpu_set_dynamics_mlp": (c_int, [c_void_p, c_int, _d, _d, _d, _d, _d, _d]),
+    "mppi_gpu_set_dynamics_basis": (c_int, [c_void_p, _d]),
     "mppi_gpu_set_costmap": (c_int, [c_void_p, c_int, _d, c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_set_costmap_f32": (c_int, [c_void_p, c_int, _P(c_float), c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_perturb_fleet_costmaps": (c_int, [c_void_p, c_double, c_uint64]),

@@ -249,7 +249,8 @@ def fp32_peak_tflops(device: int = 0):
 
 _NOISE = {"injected": _lib.NOISE_INJECTED, "ref_splitmix": _lib.NOISE_REF_SPLITMIX, "philox": _lib.NOISE_PHILOX}
 _PREC = {"fp32": _lib.FP32, "fp64": _lib.FP64}
-_SYSTEM = {"vehicle_mlp": _lib.SYSTEM_VEHICLE_MLP, "quadratic": _lib.SYSTEM_QUADRATIC}
+_SYSTEM = {"vehicle_mlp": _lib.SYSTEM_VEHICLE_MLP, "quadratic": _lib.SYSTEM_QUADRATIC,
+           "vehicle_basis": _lib.SYSTEM_VEHICLE_BASIS}
 
 
 def make_config(params: SamplingParams, bounds: ControlBounds = ControlBounds(),
@@ -332,6 +333,11 @@ class Controller:
     def set_mlp(self, w: MlpWeights) -> None:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (w.w1, w.b1, w.w2, w.b2, w.w3, w.b3)]
         check(self._lib.mppi_gpu_set_dynamics_mlp(self._h, w.hidden, *[dptr(a) for a in arrs]))
+
+    def set_basis(self, theta) -> None:
+        """BasisFunctionModel Theta (dynamics.hpp:75-82): 25 x 4, coeffs(b, o)."""
+        t = np.ascontiguousarray(theta, dtype=np.float64).reshape(25, 4)
+        check(self._lib.mppi_gpu_set_dynamics_basis(self._h, dptr(t)))
 
     def set_costmap(self, m: CostMap, controller: int = -1) -> None:
         v = m.values

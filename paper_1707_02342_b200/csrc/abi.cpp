@@ -104,6 +104,12 @@ int mppi_gpu_set_dynamics_mlp(mppi_gpu_handle* h, int hidden, const double* w1, 
     x.set_mlp(hidden, w1, b1, w2, b2, w3, b3);
   });
 }
+int mppi_gpu_set_dynamics_basis(mppi_gpu_handle* h, const double* theta) {
+  return with_handle(h, [&](auto& x) {
+    if (!theta) throw_invalid("set_dynamics_basis: null theta");
+    x.set_basis(theta);
+  });
+}
 int mppi_gpu_set_costmap(mppi_gpu_handle* h, int controller, const double* values, int width,
                          int height, double x0, double y0, double resolution) {
   return with_handle(h, [&](auto& x) {

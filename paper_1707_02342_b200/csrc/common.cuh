@@ -34,6 +34,10 @@ __device__ __forceinline__ float exp_r(float x) { return expf(x); }
 __device__ __forceinline__ double exp_r(double x) { return exp(x); }
 __device__ __forceinline__ float atan_r(float x) { return atanf(x); }
 __device__ __forceinline__ double atan_r(double x) { return atan(x); }
+__device__ __forceinline__ float tan_r(float x) { return tanf(x); }
+__device__ __forceinline__ double tan_r(double x) { return tan(x); }
+__device__ __forceinline__ float sin_r(float x) { return sinf(x); }
+__device__ __forceinline__ double sin_r(double x) { return sin(x); }
 __device__ __forceinline__ float abs_r(float x) { return fabsf(x); }
 __device__ __forceinline__ double abs_r(double x) { return fabs(x); }
 __device__ __forceinline__ void sincos_r(float x, float* s, float* c) { sincosf(x, s, c); }

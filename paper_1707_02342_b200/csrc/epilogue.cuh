@@ -91,7 +91,7 @@ __device__ __forceinline__ void epilogue_body(const EpilogueArgs<R>& a, const Ml
   StepStatus* st = a.status + ctrl;
   if (st->code != 0) return;  // sticky abort: a previous stage failed
   R* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
-  if constexpr (Sys::kHasMap) {
+  if constexpr (Sys::kMlp) {
     if (a.plant) {  // stage the plant's weights (overlaps the merge)
       const float4* src = reinterpret_cast<const float4*>(w_src);
       float4* dst = reinterpret_cast<float4*>(s_w);
@@ -195,7 +195,7 @@ __device__ __forceinline__ void epilogue_body(const EpilogueArgs<R>& a, const Ml
   if (a.plant) {
     // Device plant: the same model stepped with the executed (clamped) input.
     R* x = a.x0 + static_cast<size_t>(ctrl) * 8;
-    if constexpr (Sys::kHasMap) {
+    if constexpr (Sys::kMlp) {
       // warp-parallel MLP step: thread j owns hidden unit j
       const MlpParams<R, H>& w = *s_w;
       const R in[6] = {x[3], x[4], x[5], x[6], s_u[0], s_u[1]};
@@ -230,11 +230,11 @@ __device__ __forceinline__ void epilogue_body(const EpilogueArgs<R>& a, const Ml
         for (int i = 0; i < 7; ++i) x[i] = xs[i];
       }
     } else {
-      if (threadIdx.x == 0) {
-        R xs[7] = {x[0], x[1], R(0), R(0), R(0), R(0), R(0)};
+      if (threadIdx.x == 0) {  // quadratic fixture / basis-function model: one thread
+        R xs[7];
+        for (int i = 0; i < 7; ++i) xs[i] = (i < Sys::kStateDim) ? x[i] : R(0);
         Sys::step(xs, s_u[0], s_u[1], *w_src, a.sys);
-        x[0] = xs[0];
-        x[1] = xs[1];
+        for (int i = 0; i < Sys::kStateDim; ++i) x[i] = xs[i];
       }
     }
     __syncthreads();

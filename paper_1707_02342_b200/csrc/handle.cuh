@@ -179,7 +179,9 @@ struct Handle final : HandleBase {
     else
       std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
                     std::is_same<R, double>::value ? "f64" : "f32", H,
-                    cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic" : "vehicle_mlp", cfg.noise_mode, kBlock);
+                    cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic"
+                    : (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS ? "vehicle_basis" : "vehicle_mlp"),
+                    cfg.noise_mode, kBlock);
     return buf;
   }
 
@@ -215,6 +217,7 @@ struct Handle final : HandleBase {
 
   // weights (host copies; by-value kernel parameters) + device copy for the
   // by-pointer variant
+  ThetaDev<R> theta_r{};  // VEHICLE_BASIS coefficients
   std::unique_ptr<MlpParams<R, 32>> w32;
   std::unique_ptr<MlpParams<R, 64>> w64;
   DevBuf<MlpParams<R, 64>> d_w64;
@@ -429,7 +432,9 @@ struct Handle final : HandleBase {
       throw Error(MPPI_ERR_UNSUPPORTED, "only the information-theoretic weight rule runs on the device");
     if (c.noise_mode < 0 || c.noise_mode > 2) throw_invalid("noise_mode");
     if (c.precision != MPPI_FP32 && c.precision != MPPI_FP64) throw_invalid("precision");
-    if (c.system != MPPI_SYSTEM_VEHICLE_MLP && c.system != MPPI_SYSTEM_QUADRATIC) throw_invalid("system");
+    if (c.system != MPPI_SYSTEM_VEHICLE_MLP && c.system != MPPI_SYSTEM_QUADRATIC &&
+        c.system != MPPI_SYSTEM_VEHICLE_BASIS)
+      throw_invalid("system");
     if (c.mlp_hidden != 32 && c.mlp_hidden != 64) throw_invalid("mlp_hidden must be 32 or 64");
     if (c.n_controllers < 1) throw_invalid("n_controllers must be >= 1");
     if (c.noise_mode == MPPI_NOISE_INJECTED && c.n_controllers != 1)
@@ -452,7 +457,7 @@ struct Handle final : HandleBase {
       }
   }
   void require_ready() const {
-    if (!has_mlp) throw_invalid("vehicle system: MLP weights not set");
+    if (!has_mlp) throw_invalid("vehicle system: model (MLP weights / basis Theta) not set");
     if (!has_map) throw_invalid("vehicle system: costmap not set");
     if (cfg.noise_mode == MPPI_NOISE_INJECTED && !has_noise) throw_invalid("INJECTED noise: no batch set");
   }
@@ -499,9 +504,21 @@ struct Handle final : HandleBase {
     invalidate_graphs();
   }
 
+  // BasisFunctionModel Theta (dynamics.hpp:75-82), theta[b*4 + o]; like
+  // load_theta, non-finite entries are rejected (dynamics.cpp:240-242).
+  void set_basis(const double* theta) {
+    if (cfg.system != MPPI_SYSTEM_VEHICLE_BASIS) throw_invalid("set_dynamics_basis: system is not the basis model");
+    for (int i = 0; i < 100; ++i)
+      if (!std::isfinite(theta[i])) throw_invalid("set_dynamics_basis: non-finite Theta entry");
+    for (int b = 0; b < 25; ++b)
+      for (int o = 0; o < 4; ++o) theta_r.c[b][o] = static_cast<R>(theta[b * 4 + o]);
+    has_mlp = true;  // the model is set
+    invalidate_graphs();
+  }
+
   template <class Src>
   void set_map(int ctrl, const Src* values, int width, int height, double x0, double y0, double res) {
-    if (cfg.system != MPPI_SYSTEM_VEHICLE_MLP) throw_invalid("set_costmap: system has no costmap");
+    if (cfg.system == MPPI_SYSTEM_QUADRATIC) throw_invalid("set_costmap: system has no costmap");
     // CostMap::validate (costs.hpp:24-37)
     if (width < 2 || height < 2) throw_invalid("CostMap: width and height must be >= 2");
     if (!(res > 0.0)) throw_invalid("CostMap: resolution must be > 0");
@@ -673,6 +690,7 @@ struct Handle final : HandleBase {
     s.decay_pow = d_decay.p;
     s.with_terminal = cfg.with_terminal;
     s.quad_cost_scale = static_cast<R>(cfg.quad_cost_scale);
+    s.theta = theta_r;
     return s;
   }
   template <int HH>
@@ -701,6 +719,8 @@ struct Handle final : HandleBase {
     };
     if (cfg.system == MPPI_SYSTEM_QUADRATIC)
       by_mode(std::integral_constant<int, 32>{}, type_tag<Quadratic<R, 32>>{});
+    else if (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS)
+      by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleBasis<R, 32>>{});
     else if (H == 32)
       by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleMlp<R, 32>>{});
     else
@@ -1084,7 +1104,7 @@ struct Handle final : HandleBase {
   void rollout_costs(const double* x0, const double* eps_in, double* costs_out, double* eps_stored_out) {
     if (eps_in) upload_injected(eps_in);
     else if (cfg.noise_mode == MPPI_NOISE_INJECTED && !has_noise) throw_invalid("INJECTED noise: no batch set");
-    if (!has_mlp) throw_invalid("vehicle system: MLP weights not set");
+    if (!has_mlp) throw_invalid("vehicle system: model (MLP weights / basis Theta) not set");
     if (!has_map) throw_invalid("vehicle system: costmap not set");
     upload_x0(x0);
     CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));

@@ -178,6 +178,53 @@ __device__ __forceinline__ void advance_split(R x[7], const R d[4], R dt) {
   x[2] = n2;
 }
 
+// BasisFunctionModel coefficients (dynamics.hpp:75-82): c[b][o] = coeffs(b, o).
+template <class R>
+struct ThetaDev {
+  R c[25][4];
+};
+
+// eval_basis (dynamics.cpp:83-133), kSlipGuardSpeed = 0.1 (dynamics.cpp:47).
+template <class R>
+__device__ __forceinline__ void eval_basis(R roll, R v_x, R v_y, R r, R u_delta, R u_F, R phi[25]) {
+  R alpha_f, alpha_r, ratio;
+  if (v_x > R(0.1)) {
+    ratio = div_r(v_y, v_x);
+    alpha_f = atan_r(sub_rn(add_rn(ratio, div_r(mul_rn(R(0.45), r), v_x)), u_delta));
+    alpha_r = atan_r(sub_rn(ratio, div_r(mul_rn(R(0.35), r), v_x)));
+  } else {
+    ratio = R(0);
+    alpha_f = -u_delta;
+    alpha_r = R(0);
+  }
+  const R tf = tan_r(alpha_f), tr = tan_r(alpha_r), sd = sin_r(u_delta);
+  phi[0] = u_F;
+  phi[1] = div_r(v_x, R(10.0));
+  phi[2] = div_r(mul_rn(sd, tf), R(1200.0));
+  phi[3] = div_r(mul_rn(mul_rn(sd, tf), abs_r(tf)), R(1200.0 * 1200.0));
+  phi[4] = div_r(mul_rn(mul_rn(mul_rn(sd, tf), tf), tf), R(1200.0 * 1200.0 * 1200.0));
+  phi[5] = div_r(mul_rn(r, v_y), R(25.0));
+  phi[6] = div_r(r, R(10.0));
+  phi[7] = div_r(v_y, R(10.0));
+  phi[8] = sd;
+  phi[9] = div_r(ratio, R(40.0));
+  phi[10] = div_r(tf, R(1400.0));
+  phi[11] = div_r(mul_rn(tf, abs_r(tf)), R(1400.0 * 1400.0));
+  phi[12] = div_r(mul_rn(mul_rn(tf, tf), tf), R(1400.0 * 1400.0 * 1400.0));
+  phi[13] = div_r(tr, R(40.0));
+  phi[14] = div_r(mul_rn(tr, abs_r(tr)), R(40.0 * 40.0));
+  phi[15] = div_r(mul_rn(mul_rn(tr, tr), tr), R(40.0 * 40.0 * 40.0));
+  phi[16] = div_r(mul_rn(r, v_x), R(50.0));
+  phi[17] = roll;
+  phi[18] = mul_rn(roll, r);
+  phi[19] = div_r(mul_rn(roll, v_x), R(3.0));
+  phi[20] = div_r(mul_rn(mul_rn(roll, v_x), r), R(5.0));
+  phi[21] = div_r(mul_rn(v_x, v_x), R(100.0));
+  phi[22] = div_r(mul_rn(mul_rn(v_x, v_x), v_x), R(1000.0));
+  phi[23] = mul_rn(u_F, u_F);
+  phi[24] = mul_rn(mul_rn(u_F, u_F), u_F);
+}
+
 // Everything a rollout system needs besides the weights.
 template <class R>
 struct SystemArgs {
@@ -187,12 +234,14 @@ struct SystemArgs {
   const R* decay_pow;    // T+1 entries
   int with_terminal;
   R quad_cost_scale;
+  ThetaDev<R> theta;     // VEHICLE_BASIS coefficients
 };
 
 template <class R, int H>
 struct VehicleMlp {
   static constexpr int kStateDim = 7;
   static constexpr bool kHasMap = true;
+  static constexpr bool kMlp = true;
   // step (controller.cpp:13-20): clamp then MlpModel::step
   __device__ __forceinline__ static void step(R x[7], R v0, R v1, const MlpParams<R, H>& w,
                                               const SystemArgs<R>& a) {
@@ -203,10 +252,35 @@ struct VehicleMlp {
   }
 };
 
+// make_vehicle_system over BasisFunctionModel: clamp -> step_basis_model
+// (dynamics.cpp:152-157): xd_dot = Theta^T phi summed over the basis functions
+// in ascending order (the oracle does the same; Eigen's GEMV order is not
+// reproduced, see oracle/mppi_oracle.cpp), then advance_split.
+template <class R, int H>
+struct VehicleBasis {
+  static constexpr int kStateDim = 7;
+  static constexpr bool kHasMap = true;
+  static constexpr bool kMlp = false;
+  __device__ __forceinline__ static void step(R x[7], R v0, R v1, const MlpParams<R, H>&, const SystemArgs<R>& a) {
+    R phi[25];
+    eval_basis<R>(x[3], x[4], x[5], x[6], clamp_r(v0, a.lo0, a.hi0), clamp_r(v1, a.lo1, a.hi1), phi);
+    R d[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      R acc = mul_rn(a.theta.c[0][o], phi[0]);
+#pragma unroll
+      for (int b = 1; b < 25; ++b) acc = add_rn(acc, mul_rn(a.theta.c[b][o], phi[b]));
+      d[o] = acc;
+    }
+    advance_split<R>(x, d, a.dt);
+  }
+};
+
 template <class R, int H>
 struct Quadratic {
   static constexpr int kStateDim = 2;
   static constexpr bool kHasMap = false;
+  static constexpr bool kMlp = false;
   __device__ __forceinline__ static void step(R x[7], R v0, R v1, const MlpParams<R, H>&,
                                               const SystemArgs<R>& a) {
     x[0] = add_rn(x[0], mul_rn(v0, a.dt));

@@ -39,7 +39,26 @@ CONFIGS = {
                desc="fleet of 512 independent controllers, K=2048, T=100, perturbed maps"),
     "c4": dict(samples=(1024, 4096, 16384, 65536, 262144, 1048576), horizon_steps=100, hidden=32, controllers=1,
                desc="K sweep at T=100, H=32"),
+    # the reference's only throughput budget (acceptance criterion 10,
+    # proj/tests/acceptance.cpp:344-393): K=1024, T=100, basis-function model,
+    # dt 0.025, SG(9, 3), median mpc_step <= 100 ms on <= 8 threads.
+    "ref10": dict(samples=1024, horizon_steps=100, hidden=32, controllers=1, system="vehicle_basis",
+                  desc="reference acceptance #10: K=1024, T=100, basis-function model"),
 }
+
+
+def basis_theta(seed: int = SEED) -> np.ndarray:
+    """A seeded 25 x 4 Theta for the basis-function model.  The reference fits
+    Theta to its bicycle truth model (fit_theta, dynamics.cpp:159-195), which is
+    out of scope here; this stand-in has throttle drive and quadratic drag on
+    v_x (coeffs(0, 1) = 3, coeffs(21, 1) = -2), yaw/slip damping (coeffs(6, 3),
+    coeffs(7, 2) = -2), steering -> yaw rate (coeffs(8, 3) = 4) and
+    N(0, 0.05^2) everywhere else."""
+    rng = np.random.default_rng(seed)
+    th = 0.05 * rng.standard_normal((25, 4))
+    th[0, 1], th[21, 1] = 3.0, -2.0
+    th[6, 3], th[7, 2], th[8, 3] = -2.0, -2.0, 4.0
+    return th
 
 
 @dataclass
@@ -54,6 +73,8 @@ class Workload:
     costmap: CostMap
     x0: np.ndarray          # n_controllers x 7
     controllers: int
+    system: str = "vehicle_mlp"
+    theta: Optional[np.ndarray] = None  # vehicle_basis only
 
     def controller_kwargs(self, **kw):
         d = dict(hidden=self.hidden, n_controllers=self.controllers)
@@ -78,12 +99,17 @@ def make(name: str, samples: Optional[int] = None, horizon_steps: Optional[int] 
         K = K[0]
     T = horizon_steps if horizon_steps is not None else spec["horizon_steps"]
     C = controllers if controllers is not None else spec["controllers"]
-    params = SamplingParams(samples=int(K), horizon_steps=int(T), dt=0.02, sigma_diag=(0.3 ** 2, 0.35 ** 2),
+    system = spec.get("system", "vehicle_mlp")
+    dt = 0.025 if system == "vehicle_basis" else 0.02
+    params = SamplingParams(samples=int(K), horizon_steps=int(T), dt=dt, sigma_diag=(0.3 ** 2, 0.35 ** 2),
                             lambda_=6.66, gamma=0.1 * 6.66, explore_fraction=0.01, seed=seed)
     H = spec["hidden"]
     mlp = MlpWeights.xavier(H, seed, 0.1)
     x0 = initial_states(C, seed, 40.0, 25.0, True, (3.0, 8.0), 0.05)
-    return Workload(name, params, ControlBounds(), SGFilter(9, 2), CostParams.baseline(), H, mlp, track_map(), x0, C)
+    sg = SGFilter(9, 3) if system == "vehicle_basis" else SGFilter(9, 2)
+    theta = basis_theta(seed) if system == "vehicle_basis" else None
+    return Workload(name, params, ControlBounds(), sg, CostParams.baseline(), H, mlp, track_map(), x0, C, system,
+                    theta)
 
 
 def flops_per_sample_step(hidden: int) -> int:

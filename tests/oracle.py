@@ -45,6 +45,9 @@ _SIG = {
     "oracle_destroy": (None, [c_void_p]),
     "oracle_set_mlp": (c_int, [c_void_p, c_int, _d, _d, _d, _d, _d, _d]),
     "oracle_set_costmap": (c_int, [c_void_p, _d, c_int, c_int, c_double, c_double, c_double]),
+    "oracle_set_theta": (c_int, [c_void_p, _d]),
+    "oracle_eval_basis": (c_int, [_d, _d, _d]),
+    "oracle_step_basis": (c_int, [_d, _d, c_double, _d, _d]),
     "oracle_set_costmap_f32": (c_int, [c_void_p, POINTER(c_float), c_int, c_int, c_double, c_double, c_double]),
     "oracle_set_plan": (c_int, [c_void_p, _d]),
     "oracle_get_plan": (c_int, [c_void_p, _d]),
@@ -220,6 +223,10 @@ class OracleController:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (w.w1, w.b1, w.w2, w.b2, w.w3, w.b3)]
         chk(load().oracle_set_mlp(self.h, w.hidden, *[p(a) for a in arrs]))
 
+    def set_basis(self, theta):
+        t = np.ascontiguousarray(theta, dtype=np.float64).reshape(25, 4)
+        chk(load().oracle_set_theta(self.h, p(t)))
+
     def set_costmap(self, m):
         v = np.ascontiguousarray(m.values, dtype=np.float64)
         chk(load().oracle_set_costmap(self.h, p(v), m.width, m.height, m.x0, m.y0, m.resolution))
@@ -296,3 +303,20 @@ class OracleController:
 
 def side_slip(vx, vy):
     return float(load().oracle_side_slip(vx, vy))
+
+
+def eval_basis(x_d, v):
+    """eval_basis (dynamics.cpp:83-133) of the restatement, double."""
+    phi = np.zeros(25)
+    load().oracle_eval_basis(p(np.ascontiguousarray(x_d, dtype=np.float64)),
+                             p(np.ascontiguousarray(v, dtype=np.float64)), p(phi))
+    return phi
+
+
+def step_basis(x, v, dt, theta):
+    """step_basis_model (dynamics.cpp:152-157) of the restatement, double."""
+    out = np.zeros(7)
+    chk(load().oracle_step_basis(p(np.ascontiguousarray(x, dtype=np.float64)),
+                                 p(np.ascontiguousarray(v, dtype=np.float64)), dt,
+                                 p(np.ascontiguousarray(theta, dtype=np.float64).reshape(100)), p(out)))
+    return out
