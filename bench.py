@@ -128,8 +128,12 @@ def reference_cpu(w, steps, warmup, sample_k):
     import oracle  # test infrastructure; the CPU arm only
     from paper_1707_02342_b200.api import SamplingParams
     p = SamplingParams(**{**w.params.__dict__, "samples": sample_k})
-    o = oracle.OracleController(p, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp64", noise="ref_splitmix")
-    o.set_mlp(w.mlp)
+    o = oracle.OracleController(p, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp64", noise="ref_splitmix",
+                                system=w.system)
+    if w.theta is not None:
+        o.set_basis(w.theta)
+    else:
+        o.set_mlp(w.mlp)
     o.set_costmap(w.costmap)
     threads = cpu_threads()
     x = w.x0[0].copy()
@@ -199,8 +203,11 @@ def run_ours(args):
     # communicator; otherwise the samples of one controller are sharded
     C = max(1, w.controllers // world) if fleet else 1
     ctrl = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox",
-                      device=local, n_controllers=C)
-    ctrl.set_mlp(w.mlp)
+                      device=local, n_controllers=C, system=w.system)
+    if w.theta is not None:
+        ctrl.set_basis(w.theta)
+    else:
+        ctrl.set_mlp(w.mlp)
     ctrl.set_costmap(w.costmap)
     if fleet:
         ctrl.perturb_fleet_costmaps(0.02, workload.SEED + rank)  # per-controller N(0, 0.02^2) map noise
@@ -269,7 +276,8 @@ def run_ours(args):
             pg.destroy_process_group()
         return
 
-    flop_unit = workload.flops_per_sample_step(w.hidden)
+    # algorithmic FLOPs per sample-step: the MLP GEMVs, or Theta^T phi (25 x 4) of the basis model
+    flop_unit = 2 * 25 * 4 if w.theta is not None else workload.flops_per_sample_step(w.hidden)
     k_local = K * C if fleet else (K // world if world > 1 else K)
     k1_flops = k_local * T * flop_unit
     peak, clk = fp32_peak_tflops(local)
@@ -285,7 +293,9 @@ def run_ours(args):
         # fleet) is fixed and split over the GPUs
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Xavier MLP, 2000x2000 ellipse map, Philox noise)",
-        "config": {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, H={w.hidden}, MLP vehicle, "
+        "config": {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, "
+                               + ("basis-function vehicle (reference acceptance #10 shape), "
+                                  if w.theta is not None else f"H={w.hidden}, MLP vehicle, ") +
                                f"receding horizon with device plant"
                                + (f", fleet of {C * world} controllers (perturbed maps)" if fleet else ""),
                    "samples": K, "horizon": T, "hidden": w.hidden, "controllers": C * world,

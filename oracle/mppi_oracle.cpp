@@ -577,6 +577,31 @@ Weights<R> it_weights(const std::vector<R>& costs, R lambda) {
   return r;
 }
 
+// cem_weights (weights.cpp:27-53): the lround(K (1 - delta)) lowest costs,
+// ties broken by ascending sample index, each weighted 1 / elite.
+template <class R>
+Weights<R> cem_weights(const std::vector<R>& costs, double delta) {
+  const int K = static_cast<int>(costs.size());
+  if (K < 1) throw std::invalid_argument("cem_weights: need at least one cost");
+  if (!(delta > 0.0 && delta < 1.0)) throw std::invalid_argument("cem_weights: delta must be in (0, 1)");
+  for (R c : costs)
+    if (!std::isfinite(c)) throw NonFinite("cem_weights: non-finite cost");
+  const int elite = static_cast<int>(std::lround(K * (1.0 - delta)));
+  if (elite < 1) throw std::invalid_argument("cem_weights: delta leaves an empty elite set");
+  std::vector<int> order(K);
+  for (int k = 0; k < K; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    if (costs[a] != costs[b]) return costs[a] < costs[b];
+    return a < b;
+  });
+  Weights<R> r;
+  r.rho = costs[order.front()];
+  r.normalizer = static_cast<R>(elite);
+  r.w.assign(K, R(0));
+  for (int i = 0; i < elite; ++i) r.w[order[i]] = R(1) / static_cast<R>(elite);
+  return r;
+}
+
 // ControllerState (controller.hpp:40-58) + the data the device handle owns.
 template <class R>
 struct Controller {
@@ -688,12 +713,18 @@ struct Controller {
     return out;
   }
 
+  // compute_weights (controller.cpp:111-116): IT or CEM by the weight rule.
+  Weights<double> compute_weights(const std::vector<double>& costs) const {
+    if (cfg.weight_rule == MPPI_WEIGHT_CEM) return cem_weights<double>(costs, cfg.cem_delta);
+    return it_weights<double>(costs, p.lambda);
+  }
+
   // mpc_step (controller.cpp:133-148)
   void mpc_step(const R* x0, R u0[2], int n_threads) {
     const System<R> sys = system();
     Batch<R> batch = sample(iteration);
     const std::vector<double> costs = rollout_batch(sys, x0, batch, n_threads);
-    const Weights<double> w = it_weights<double>(costs, p.lambda);
+    const Weights<double> w = compute_weights(costs);
     plan = update_plan(batch, w.w);
     for (int c = 0; c < 2; ++c) u0[c] = clampv(plan[c], lo[c], hi[c]);
     const int T = p.horizon_steps;
@@ -712,7 +743,7 @@ struct Controller {
     for (int i = 0; i < iterations; ++i) {
       Batch<R> batch = sample(iteration);
       const std::vector<double> costs = rollout_batch(sys, x0, batch, n_threads);
-      const Weights<double> w = it_weights<double>(costs, p.lambda);
+      const Weights<double> w = compute_weights(costs);
       plan = update_plan(batch, w.w);
       ++iteration;
     }
@@ -861,6 +892,15 @@ int oracle_it_weights(const double* costs, int K, double lambda, double* w_out, 
   return orc::guard([&] {
     std::vector<double> c(costs, costs + std::max(K, 0));
     const auto r = orc::it_weights<double>(c, lambda);
+    std::copy(r.w.begin(), r.w.end(), w_out);
+    *rho = r.rho;
+    *eta = r.normalizer;
+  });
+}
+int oracle_cem_weights(const double* costs, int K, double delta, double* w_out, double* rho, double* eta) {
+  return orc::guard([&] {
+    std::vector<double> c(costs, costs + std::max(K, 0));
+    const auto r = orc::cem_weights<double>(c, delta);
     std::copy(r.w.begin(), r.w.end(), w_out);
     *rho = r.rho;
     *eta = r.normalizer;
@@ -1063,7 +1103,7 @@ int oracle_weights(AnyController* h, const double* costs, double* w_out, double*
                    double* eta) {
   return orc::dispatch(h, [&](auto& c) {
     std::vector<double> s(costs, costs + c.p.samples);
-    const auto r = orc::it_weights<double>(s, c.p.lambda);
+    const auto r = c.compute_weights(s);
     for (size_t k = 0; k < r.w.size(); ++k) w_out[k] = r.w[k];
     *rho = r.rho;
     *eta = r.normalizer;

@@ -257,7 +257,11 @@ def make_config(params: SamplingParams, bounds: ControlBounds = ControlBounds(),
                 sg: Optional[SGFilter] = SGFilter(), cost: CostParams = CostParams(), *,
                 system: str = "vehicle_mlp", hidden: int = 32, precision: str = "fp32",
                 noise: str = "philox", n_controllers: int = 1, device: int = 0,
-                with_terminal: bool = True, quad_cost_scale: float = 1.0) -> _lib.ConfigC:
+                with_terminal: bool = True, quad_cost_scale: float = 1.0, weight_rule: str = "it",
+                cem_delta: float = 0.8) -> _lib.ConfigC:
+    """mppi_gpu_config from the reference's parameter objects; ``weight_rule``
+    "it" (it_weights) or "cem" (cem_weights with ``cem_delta``, the
+    WeightRuleConfig of controller.hpp:32-37)."""
     cfg = _lib.ConfigC()
     _lib.load().mppi_gpu_config_init(ctypes.byref(cfg))
     sig = list(params.sigma_diag)
@@ -283,6 +287,8 @@ def make_config(params: SamplingParams, bounds: ControlBounds = ControlBounds(),
     cfg.n_controllers = n_controllers
     cfg.device = device
     cfg.quad_cost_scale = quad_cost_scale
+    cfg.weight_rule = {"it": _lib.WEIGHT_IT, "cem": _lib.WEIGHT_CEM}[weight_rule]
+    cfg.cem_delta = cem_delta
     for f in CostParams.__dataclass_fields__:
         setattr(cfg.cost, f, float(getattr(cost, f)))
     return cfg
@@ -444,7 +450,7 @@ class Controller:
         return (costs, stored) if return_batch else costs
 
     def compute_weights(self, costs) -> WeightResult:
-        """compute_weights -> it_weights (weights.cpp:8-25)."""
+        """compute_weights (controller.cpp:111-116): it_weights (weights.cpp:8-25) or cem_weights (:27-53)."""
         c = np.ascontiguousarray(costs, dtype=np.float64)
         if c.size != self.K:
             raise InvalidArgument(_lib.MPPI_ERR_INVALID_ARGUMENT, "costs must have K entries")

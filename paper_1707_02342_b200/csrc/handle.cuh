@@ -21,6 +21,7 @@
 
 #include "epilogue.cuh"
 #include "rollout_tc.cuh"
+#include "cem.cuh"
 #include "ws_launch.hpp"
 #include "errors.hpp"
 #include "handle_iface.hpp"
@@ -290,6 +291,7 @@ struct Handle final : HandleBase {
     d_x0.alloc(static_cast<size_t>(C) * 8);
     CUDA_TRY(cudaMemset(d_x0.p, 0, d_x0.n * sizeof(R)));
     d_costs.alloc(static_cast<size_t>(C) * K);
+    if (c.weight_rule == MPPI_WEIGHT_CEM) d_w.alloc(K);  // (allocated before any graph capture)
     d_partials.alloc(static_cast<size_t>(C) * partials_ctrl_stride);
     setup_merge();
     setup_tail();
@@ -428,8 +430,13 @@ struct Handle final : HandleBase {
       if (c.sg_degree < 0 || c.sg_degree >= c.sg_window) throw_invalid("sg_coefficients: need 0 <= degree < window");
       if (c.sg_window > kMaxSgWindow) throw Error(MPPI_ERR_UNSUPPORTED, "sg window > 63");
     }
-    if (c.weight_rule != MPPI_WEIGHT_IT)
-      throw Error(MPPI_ERR_UNSUPPORTED, "only the information-theoretic weight rule runs on the device");
+    if (c.weight_rule != MPPI_WEIGHT_IT && c.weight_rule != MPPI_WEIGHT_CEM) throw_invalid("weight_rule");
+    if (c.weight_rule == MPPI_WEIGHT_CEM) {  // cem_weights (weights.cpp:27-40)
+      if (!(c.cem_delta > 0.0 && c.cem_delta < 1.0)) throw_invalid("cem_weights: delta must be in (0, 1)");
+      if (std::lround(c.samples * (1.0 - c.cem_delta)) < 1)
+        throw_invalid("cem_weights: delta leaves an empty elite set");
+      if (c.n_controllers != 1) throw Error(MPPI_ERR_UNSUPPORTED, "the CEM rule runs one controller per handle");
+    }
     if (c.noise_mode < 0 || c.noise_mode > 2) throw_invalid("noise_mode");
     if (c.precision != MPPI_FP32 && c.precision != MPPI_FP64) throw_invalid("precision");
     if (c.system != MPPI_SYSTEM_VEHICLE_MLP && c.system != MPPI_SYSTEM_QUADRATIC &&
@@ -799,6 +806,27 @@ struct Handle final : HandleBase {
   // epilogue over the merged row — identical arithmetic either way.  Other
   // K1 variants: K1, exchange, pre-merge, epilogue.
   void enqueue_iteration(int mode, bool events, bool slide, bool increment, bool plant, bool trace) {
+    if (cfg.weight_rule == MPPI_WEIGHT_CEM) {
+      // CEM (controller.cpp:111-116 -> weights.cpp:27-53): K1 for the costs,
+      // the device elite selection, update_plan with those weights
+      // (ascending-k weighted sum over the regenerated batch), the epilogue
+      enqueue_rollout(mode, events);
+      cem_weights_kernel<1024><<<1, 1024, 0, stream>>>(d_costs.p, K, cem_elite(), d_w.p, d_rho_eta.p, nullptr,
+                                                        d_status.p);
+      ++launches;
+      CUDA_TRY(cudaGetLastError());
+      const RolloutArgs<R> a = rollout_args();
+      const int blocks = (T + 127) / 128;
+      switch (mode) {
+        case kInjected: weighted_agg_kernel<R, kInjected><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+        case kRefSplitmix: weighted_agg_kernel<R, kRefSplitmix><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+        default: weighted_agg_kernel<R, kPhilox><<<blocks, 128, 0, stream>>>(a, d_w.p, d_agg.p); break;
+      }
+      ++launches;
+      CUDA_TRY(cudaGetLastError());
+      enqueue_epilogue(false, slide, increment, plant, trace, 1);
+      return;
+    }
     if (use_tc) {
       if constexpr (std::is_same<R, float>::value) {
         if (coop_tail()) {
@@ -1137,12 +1165,17 @@ struct Handle final : HandleBase {
 
   // it_weights on caller costs; the softmin runs in double for every
   // precision (Acc, rollout.cuh), as in the fused path.
+  int cem_elite() const { return static_cast<int>(std::lround(K * (1.0 - cfg.cem_delta))); }
+
   void weights(const double* costs, double* w_out, double* rho, double* eta) {
     DevBuf<Acc> d_c;
     d_c.alloc(K);
     d_w.alloc(K);
     CUDA_TRY(cudaMemcpyAsync(d_c.p, costs, K * sizeof(Acc), cudaMemcpyHostToDevice, stream));
-    weights_kernel<Acc, 1024><<<1, 1024, 0, stream>>>(d_c.p, K, cfg.lambda, d_w.p, d_rho_eta.p, d_bad.p);
+    if (cfg.weight_rule == MPPI_WEIGHT_CEM)  // compute_weights (controller.cpp:111-116)
+      cem_weights_kernel<1024><<<1, 1024, 0, stream>>>(d_c.p, K, cem_elite(), d_w.p, d_rho_eta.p, d_bad.p, nullptr);
+    else
+      weights_kernel<Acc, 1024><<<1, 1024, 0, stream>>>(d_c.p, K, cfg.lambda, d_w.p, d_rho_eta.p, d_bad.p);
     ++launches;
     CUDA_TRY(cudaGetLastError());
     int bad = 0;
@@ -1151,7 +1184,9 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaMemcpyAsync(re, d_rho_eta.p, 2 * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaMemcpyAsync(w_out, d_w.p, K * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
-    if (bad) throw Error(MPPI_ERR_NONFINITE, "it_weights: non-finite cost");
+    if (bad)
+      throw Error(MPPI_ERR_NONFINITE,
+                  cfg.weight_rule == MPPI_WEIGHT_CEM ? "cem_weights: non-finite cost" : "it_weights: non-finite cost");
     *rho = re[0];
     *eta = re[1];
   }
@@ -1226,6 +1261,8 @@ struct Handle final : HandleBase {
   void set_comm(int r, int w, const unsigned char id[128]) {
     if (w < 1 || r < 0 || r >= w) throw_invalid("set_comm: bad rank/world_size");
     if (C != 1) throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: fleets shard controllers, not samples");
+    if (cfg.weight_rule == MPPI_WEIGHT_CEM && w > 1)
+      throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: the CEM rule needs every cost on one device");
     if (comm) {
       nccl().CommDestroy(comm);
       comm = nullptr;

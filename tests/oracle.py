@@ -32,6 +32,7 @@ _SIG = {
     "oracle_sg_coefficients": (c_int, [c_int, c_int, _d]),
     "oracle_sg_smooth": (c_int, [_d, c_int, c_int, _d, c_int, _d]),
     "oracle_it_weights": (c_int, [_d, c_int, c_double, _d, _d, _d]),
+    "oracle_cem_weights": (c_int, [_d, c_int, c_double, _d, _d, _d]),
     "oracle_it_weights_f32": (c_int, [POINTER(c_float), c_int, c_float, POINTER(c_float), POINTER(c_float),
                                       POINTER(c_float)]),
     "oracle_mlp_forward": (c_int, [c_int, _d, _d, _d, _d, _d, _d, _d, _d]),
@@ -153,6 +154,15 @@ def it_weights(costs, lam):
     w = np.zeros(c.size)
     rho, eta = c_double(), c_double()
     chk(load().oracle_it_weights(p(c), c.size, lam, p(w), ctypes.byref(rho), ctypes.byref(eta)))
+    return w, rho.value, eta.value
+
+
+def cem_weights(costs, delta):
+    """cem_weights (weights.cpp:27-53) of the restatement: (weights, rho, normalizer)."""
+    c = np.ascontiguousarray(costs, dtype=np.float64)
+    w = np.zeros(len(c))
+    rho, eta = c_double(), c_double()
+    chk(load().oracle_cem_weights(p(c), len(c), delta, p(w), ctypes.byref(rho), ctypes.byref(eta)))
     return w, rho.value, eta.value
 
 
