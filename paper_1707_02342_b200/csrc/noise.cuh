@@ -60,16 +60,32 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 
 // Box-Muller of one Philox half-draw: u1 = ((a>>8)+1) 2^-24 in (0,1],
 // u2 = (b>>8) 2^-24 in [0,1) (both exact in fp32).
+//
+// fp32 (the production noise of the fp32 kernels) on the SFU, branch-free:
+//  * -ln(u1): MUFU.LG2 * ln 2, except within 2^-6 of 1 where its absolute
+//    error (~2^-22) would dominate the small result; there the series
+//    x + x^2/2 + x^3/3 + x^4/4 of x = 1 - u1 (exact) is used;
+//  * r = sqrt.approx(2 (-ln u1));
+//  * (cos, sin)(2 pi u2) = -(cos, sin)(2 pi u2 - pi): MUFU.SIN/COS on [-pi, pi)
+//    (abs. error ~2^-21).
+// Every draw stays within ~1e-6 of the double-precision Box-Muller of the same
+// integers (the oracle's definition, checked by the Philox parity test).
 __device__ __forceinline__ void philox_box_muller(uint32_t a, uint32_t b, float& z0, float& z1) {
   const float u1 = static_cast<float>((a >> 8) + 1u) * 0x1.0p-24f;
   const float u2 = static_cast<float>(b >> 8) * 0x1.0p-24f;
-  // sqrt.approx (MUFU, ~1 ulp): no IEEE slow-path branch in the rollout loop
+  const float x = 1.0f - u1;  // exact: u1 is a multiple of 2^-24 in (0, 1]
+  const float series = x * __fmaf_rn(x, __fmaf_rn(x, __fmaf_rn(x, 0.25f, 0.33333334f), 0.5f), 1.0f);
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u1));
+  const float nlog = (x < 0.015625f) ? series : -0.69314718f * lg;
   float r;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-2.0f * logf(u1)));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(2.0f * nlog));
+  const float phi = __fmaf_rn(u2, 6.28318531f, -3.14159265f);
   float s, c;
-  sincospif(2.0f * u2, &s, &c);
-  z0 = r * c;
-  z1 = r * s;
+  asm("sin.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(phi));
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(phi));
+  z0 = -r * c;
+  z1 = -r * s;
 }
 __device__ __forceinline__ void philox_box_muller(uint32_t a, uint32_t b, double& z0, double& z1) {
   const double u1 = static_cast<double>((a >> 8) + 1u) * 0x1.0p-24;
