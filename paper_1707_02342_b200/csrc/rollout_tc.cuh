@@ -322,6 +322,10 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
   const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
   __syncthreads();  // s_plan, stage constants
+  // a one-wave grid (the on-chip eps' variant) lets its dependent tail kernel
+  // launch now: the tail's CTAs wait in cudaGridDependencySynchronize for
+  // this grid's completion, but their launch latency is hidden
+  if constexpr (STORE) cudaTriggerProgrammaticLaunchCompletion();
 
   // Noise: Philox draws one 128-bit block per step pair; the other modes (parity)
   // go through the generic per-step stream.

@@ -149,7 +149,6 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
   MlpParams<float, H>* s_w = reinterpret_cast<MlpParams<float, H>*>(
       (reinterpret_cast<uintptr_t>(s_new + 2 * T) + 15) & ~uintptr_t(15));
   __shared__ int s_code;
-  __shared__ double s_eta;
   StepStatus* st = a.status + ctrl;
   float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
   // ---- phase 1: all global reads
@@ -157,10 +156,10 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     int code = __ldcg(&st->code);
     if (code == 0 && __ldcg(row + 2) != 0.0) code = 2;  // it_weights: non-finite cost (weights.cpp:12)
     s_code = code;
-    s_eta = __ldcg(row + 1);
   }
+  const double eta_l = __ldcg(row + 1);
   for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock) {
-    s_agg[i] = __ldcg(row + kPartialHeader + i);
+    s_agg[i] = __ldcg(row + kPartialHeader + i) / eta_l;  // agg = num / eta, once per element
     s_plan[i] = plan[i];
   }
   if (a.plant) {
@@ -176,7 +175,6 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     if (threadIdx.x == 0 && __ldcg(&st->code) == 0) st->code = s_code;
     return;
   }
-  const double eta = s_eta;
   // ---- SG smoothing of agg, U' = U + SG(agg)
   const int half = a.sg_window / 2;
   int nonfinite = 0;
@@ -186,10 +184,10 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     if (a.sg_window > 0) {
       Acc acc = 0.0;
       for (int j = -half; j <= half; ++j)
-        acc = __dadd_rn(acc, __dmul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c] / eta));
+        acc = __dadd_rn(acc, __dmul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c]));
       v = acc;
     } else {
-      v = s_agg[i] / eta;
+      v = s_agg[i];
     }
     const float nv = static_cast<float>(__dadd_rn(static_cast<Acc>(s_plan[i]), v));
     nonfinite |= !isfinite(nv);
@@ -277,6 +275,9 @@ __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict
                                                            unsigned* counters, const __grid_constant__ TailArgs ta) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned s_ticket;
+  // launched as a programmatic dependent of K1 (tc_launch.cuh): the CTAs may
+  // be resident before K1 ends; everything below reads K1's output
+  cudaGridDependencySynchronize();
   const int ctrl = blockIdx.y;
   Acc* row = merged + static_cast<size_t>(ctrl) * stride;
   merge_elements<kMergeBlock>(partials + static_cast<size_t>(ctrl) * ctrl_stride, n, stride, lambda, row, blockIdx.x,

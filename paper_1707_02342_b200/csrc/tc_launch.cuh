@@ -103,9 +103,19 @@ cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, lon
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  const dim3 grid(std::min(stride, 296), ctrls);
-  kern<<<grid, mppi_dev::kMergeBlock, smem, stream>>>(partials, n, stride, ctrl_stride, lambda, merged, counters, ta);
-  return cudaGetLastError();
+  // programmatic dependent launch: the tail may launch before the previous
+  // kernel (K1 or the pre-merge) ends and waits for it on the device
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::min(stride, 296), ctrls);
+  cfg.blockDim = dim3(mppi_dev::kMergeBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, partials, n, stride, ctrl_stride, lambda, merged, counters, ta);
 }
 
 template <int H>
