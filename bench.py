@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -252,15 +253,23 @@ def run_ours(args):
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
+        dt = w.params.dt
         for _ in range(args.steps):
             u = np.asarray(ctrl.mpc_step(x)).reshape(C, 2)
             # host plant (outside the controller): kinematic pose update, the
-            # executed throttle nudges v_x
-            px, py, th, vx, vy = x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy(), x[:, 4].copy(), x[:, 5].copy()
-            x[:, 0] = px + (np.cos(th) * vx - np.sin(th) * vy) * w.params.dt
-            x[:, 1] = py + (np.sin(th) * vx + np.cos(th) * vy) * w.params.dt
-            x[:, 2] = th + x[:, 6] * w.params.dt
-            x[:, 4] = vx + 0.5 * u[:, 1] * w.params.dt
+            # executed throttle nudges v_x (scalar math for one controller)
+            if C == 1:
+                r = x[0]
+                px, py, th, vx, vy, thd = float(r[0]), float(r[1]), float(r[2]), float(r[4]), float(r[5]), float(r[6])
+                c, s_ = math.cos(th), math.sin(th)
+                r[0], r[1], r[2] = px + (c * vx - s_ * vy) * dt, py + (s_ * vx + c * vy) * dt, th + thd * dt
+                r[4] = vx + 0.5 * float(u[0, 1]) * dt
+            else:
+                px, py, th, vx, vy = x[:, 0].copy(), x[:, 1].copy(), x[:, 2].copy(), x[:, 4].copy(), x[:, 5].copy()
+                x[:, 0] = px + (np.cos(th) * vx - np.sin(th) * vy) * dt
+                x[:, 1] = py + (np.sin(th) * vx + np.cos(th) * vy) * dt
+                x[:, 2] = th + x[:, 6] * dt
+                x[:, 4] = vx + 0.5 * u[:, 1] * dt
         ev1.record(stream)
         ev1.synchronize()
         e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
