@@ -19,6 +19,8 @@
 
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "epilogue.cuh"
 
 namespace mppi_dev {
@@ -76,7 +78,11 @@ __device__ void merge_elements(const Acc* P, int n, int stride, double lambda, A
   bad = __syncthreads_or(bad);
   Acc rho = s_part[0];
   for (int w = 1; w < BLOCK / 32; ++w) rho = (s_part[w] < rho) ? s_part[w] : rho;
-  for (int r = threadIdx.x; r < n; r += BLOCK) s_scale[r] = exp(-(s_scale[r] - rho) / lambda);
+  // scale of row r, e^{-(rho_r - rho)/lambda} (fp32 SFU exp of the double
+  // argument: ~1e-7 relative, deterministic, against ~1e-5 update tolerances)
+  const double inv_lambda = 1.0 / lambda;
+  for (int r = threadIdx.x; r < n; r += BLOCK)
+    s_scale[r] = static_cast<double>(__expf(static_cast<float>(-(s_scale[r] - rho) * inv_lambda)));
   __syncthreads();
   if (e0 == 0 && threadIdx.x == 0) {
     merged[0] = rho;
@@ -136,40 +142,57 @@ __host__ __device__ constexpr size_t merge_smem_bytes(int n) {
 // is that of epilogue_kernel).  smem: fast_epilogue_smem_bytes<H>(T).
 template <int H>
 __host__ __device__ constexpr size_t fast_epilogue_smem_bytes(int T) {
-  return sizeof(double) * 2 * T + sizeof(float) * (4 * T) + sizeof(MlpParams<float, H>) + 32;
+  return sizeof(double) * 2 * T + sizeof(float) * 2 * T;  // agg + U' (reuses the merge scratch)
+}
+// What every tail CTA fetches before waiting for K1 (none of it is written by
+// K1): the plan, the plant state and the model weights.  smem: tail_pre_bytes.
+template <int H>
+__host__ __device__ constexpr size_t tail_pre_bytes(int T) {
+  return ((sizeof(float) * (2 * T + 8) + 15) & ~size_t(15)) + sizeof(MlpParams<float, H>);
 }
 template <int H>
-__device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* row,
-                                           const MlpParams<float, H>* w_src, int ctrl, unsigned char* smem) {
-  constexpr int U = H / 32;  // hidden units per lane
+__device__ __forceinline__ void tail_prefetch(const EpilogueArgs<float>& a, const MlpParams<float, H>* w_src, int ctrl,
+                                              unsigned char* pre) {
   const int T = a.T;
-  double* s_agg = reinterpret_cast<double*>(smem);
-  float* s_plan = reinterpret_cast<float*>(s_agg + 2 * T);
-  float* s_new = s_plan + 2 * T;
-  MlpParams<float, H>* s_w = reinterpret_cast<MlpParams<float, H>*>(
-      (reinterpret_cast<uintptr_t>(s_new + 2 * T) + 15) & ~uintptr_t(15));
-  __shared__ int s_code;
-  StepStatus* st = a.status + ctrl;
-  float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
-  // ---- phase 1: all global reads
-  if (threadIdx.x == 0) {
-    int code = __ldcg(&st->code);
-    if (code == 0 && __ldcg(row + 2) != 0.0) code = 2;  // it_weights: non-finite cost (weights.cpp:12)
-    s_code = code;
-  }
-  const double eta_l = __ldcg(row + 1);
-  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock) {
-    s_agg[i] = __ldcg(row + kPartialHeader + i) / eta_l;  // agg = num / eta, once per element
-    s_plan[i] = plan[i];
-  }
+  float* s_plan = reinterpret_cast<float*>(pre);
+  float* s_x = s_plan + 2 * T;
+  MlpParams<float, H>* s_w =
+      reinterpret_cast<MlpParams<float, H>*>(pre + ((sizeof(float) * (2 * T + 8) + 15) & ~size_t(15)));
+  const float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
+  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock) s_plan[i] = plan[i];
+  if (threadIdx.x < 8) s_x[threadIdx.x] = a.x0[static_cast<size_t>(ctrl) * 8 + threadIdx.x];
   if (a.plant) {
     const float4* src = reinterpret_cast<const float4*>(w_src);
     float4* dst = reinterpret_cast<float4*>(s_w);
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(MlpParams<float, H>) / 16); i += kMergeBlock)
       dst[i] = src[i];
   }
-  float xs_lane = 0.f;  // warp 0: lane i < 8 holds x[i]
-  if (a.plant && threadIdx.x < 8) xs_lane = a.x0[static_cast<size_t>(ctrl) * 8 + threadIdx.x];
+}
+template <int H>
+__device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* row, int ctrl,
+                                              unsigned char* smem, const unsigned char* pre) {
+  constexpr int U = H / 32;  // hidden units per lane
+  const int T = a.T;
+  double* s_agg = reinterpret_cast<double*>(smem);
+  float* s_new = reinterpret_cast<float*>(s_agg + 2 * T);
+  const float* s_plan = reinterpret_cast<const float*>(pre);
+  const float* s_x = s_plan + 2 * T;
+  const MlpParams<float, H>* s_w =
+      reinterpret_cast<const MlpParams<float, H>*>(pre + ((sizeof(float) * (2 * T + 8) + 15) & ~size_t(15)));
+  __shared__ int s_code;
+  __shared__ double s_sg[kMaxSgWindow];
+  for (int j = threadIdx.x; j < a.sg_window; j += kMergeBlock) s_sg[j] = a.sg[j];
+  StepStatus* st = a.status + ctrl;
+  float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
+  // ---- phase 1: the merged row and the status (the rest was prefetched)
+  if (threadIdx.x == 0) {
+    int code = __ldcg(&st->code);
+    if (code == 0 && __ldcg(row + 2) != 0.0) code = 2;  // it_weights: non-finite cost (weights.cpp:12)
+    s_code = code;
+  }
+  const double eta_l = __ldcg(row + 1);
+  for (int i = threadIdx.x; i < 2 * T; i += kMergeBlock)
+    s_agg[i] = __ldcg(row + kPartialHeader + i) / eta_l;  // agg = num / eta, once per element
   __syncthreads();
   if (s_code != 0) {
     if (threadIdx.x == 0 && __ldcg(&st->code) == 0) st->code = s_code;
@@ -183,8 +206,13 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     Acc v;
     if (a.sg_window > 0) {
       Acc acc = 0.0;
-      for (int j = -half; j <= half; ++j)
-        acc = __dadd_rn(acc, __dmul_rn(a.sg[j + half], s_agg[reflect_index(t + j, T) * 2 + c]));
+      for (int j = -half; j <= half; ++j) {
+        // reflect_index (smoothing.cpp:37-44); one mirror suffices inside the
+        // interior, the loop form only when the window exceeds the horizon
+        int idx = t + j;
+        if (idx < 0 || idx >= T) idx = reflect_index(idx, T);
+        acc = __dadd_rn(acc, __dmul_rn(s_sg[j + half], s_agg[idx * 2 + c]));
+      }
       v = acc;
     } else {
       v = s_agg[i];
@@ -217,7 +245,7 @@ __device__ __noinline__ void epilogue_fast(const EpilogueArgs<float>& a, const A
     const MlpParams<float, H>& w = *s_w;
     float x[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = __shfl_sync(0xffffffffu, xs_lane, i);
+    for (int i = 0; i < 8; ++i) x[i] = s_x[i];
     const float in[6] = {x[3], x[4], x[5], x[6], u0, u1};
     float h1[U], h2[U];
 #pragma unroll
@@ -275,8 +303,13 @@ __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict
                                                            unsigned* counters, const __grid_constant__ TailArgs ta) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned s_ticket;
-  // launched as a programmatic dependent of K1 (tc_launch.cuh): the CTAs may
-  // be resident before K1 ends; everything below reads K1's output
+  const size_t m0 = merge_smem_bytes(n), m1 = fast_epilogue_smem_bytes<H>(ta.e.T);
+  const size_t scratch = ((m0 > m1 ? m0 : m1) + 15) & ~size_t(15);
+  unsigned char* pre = smem_raw + scratch;
+  // plan, plant state and weights are not written by K1: fetch them while K1
+  // may still be running (this kernel is its programmatic dependent)
+  tail_prefetch<H>(ta.e, static_cast<const MlpParams<float, H>*>(ta.plant_w), blockIdx.y, pre);
+  // everything below reads K1's output
   cudaGridDependencySynchronize();
   const int ctrl = blockIdx.y;
   Acc* row = merged + static_cast<size_t>(ctrl) * stride;
@@ -289,7 +322,7 @@ __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
   if (threadIdx.x == 0) counters[ctrl] = 0;
-  epilogue_fast<H>(ta.e, row, static_cast<const MlpParams<float, H>*>(ta.plant_w), ctrl, smem_raw);
+  epilogue_fast<H>(ta.e, row, ctrl, smem_raw, pre);
 }
 
 }  // namespace mppi_dev

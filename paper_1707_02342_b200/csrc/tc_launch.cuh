@@ -97,7 +97,9 @@ template <int H>
 cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
                            mppi_dev::Acc* merged, unsigned* counters, const mppi_dev::TailArgs& ta, int ctrls,
                            cudaStream_t stream) {
-  const size_t smem = std::max(mppi_dev::merge_smem_bytes(n), mppi_dev::fast_epilogue_smem_bytes<H>(ta.e.T));
+  const size_t smem = ((std::max(mppi_dev::merge_smem_bytes(n), mppi_dev::fast_epilogue_smem_bytes<H>(ta.e.T)) + 15) &
+                       ~size_t(15)) +
+                      mppi_dev::tail_pre_bytes<H>(ta.e.T);
   auto kern = mppi_dev::tail_kernel<H>;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
