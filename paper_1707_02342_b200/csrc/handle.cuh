@@ -74,7 +74,7 @@ constexpr int kBlock = 128;      // samples per chunk / K1 CTA
 
 // Per-lane mma.sync fragment table of the tensor-core rollout
 // (rollout_tc.cuh, word map there): weights folded with the tanh identity
-// tanh(z) = 1 - 2 / (1 + 2^(kz)), k = 2 log2 e, then split hi/lo in fp16.
+// tanh(z) = 1 + 2s, s = -1 / (1 + 2^(kz)), k = 2 log2 e, then split hi/lo in fp16.
 template <class R, int H>
 std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
   using L = mppi_dev::TcLayout<H>;
@@ -87,8 +87,9 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
     if (kin == 6) return kk2 * static_cast<double>(w.b1[n]);
     return 0.0;
   };
-  auto B2 = [&](int i, int n) -> double { return -2.0 * kk2 * W2(n, i); };
-  auto B3 = [&](int i, int n) -> double { return n < 4 ? -2.0 * W3(n, i) : 0.0; };
+  // the layer inputs are s = -1/(1 + 2^(kz)) = (tanh z - 1) / 2
+  auto B2 = [&](int i, int n) -> double { return 2.0 * kk2 * W2(n, i); };
+  auto B3 = [&](int i, int n) -> double { return n < 4 ? 2.0 * W3(n, i) : 0.0; };
   auto hl = [](double x, int which) -> uint16_t {
     const __half h = __double2half(x);
     if (which == 0) return __half_as_ushort(h);

@@ -16,9 +16,9 @@
 // tensor core accumulates in fp32, so the MLP error is of the order of an fp32
 // FMA evaluation (checked against the float restatement in the parity tests).
 // tanh is folded into the layers: with k = 2 log2(e),
-//   tanh(z) = 1 - 2 r,  r = 1 / (1 + 2^(k z)),
+//   tanh(z) = 1 + 2 s,  s = -1 / (1 + 2^(k z)),
 // so layer 1 multiplies by k*W1 (bias k*b1 through a constant-one input),
-// layer 2 by -2k*W2 with bias k*(b2 + W2 1), layer 3 by -2*W3 with bias
+// layer 2 by 2k*W2 with bias k*(b2 + W2 1), layer 3 by 2*W3 with bias
 // b3 + W3 1, and each activation costs one ex2, one add and one rcp.
 //
 // Layout (per warp, MT m16 tiles = 16*MT samples = one chunk):
@@ -69,6 +69,14 @@ __device__ __forceinline__ void mma_k16(float (&d)[4], const uint32_t (&a)[4], u
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// D = A B + C with C left intact (a bias quad feeds the first product directly)
+__device__ __forceinline__ void mma_k16_c(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                          const float (&c)[4]) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]), "f"(c[3]));
+}
+
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 // (x, y) -> fp16x2 hi and lo words: hi = fp16(x), lo = fp16(x - hi).
@@ -90,17 +98,57 @@ __device__ __forceinline__ float tc_rcp(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// r = 1 / (1 + 2^y) on a pair (tanh(z) = 1 - 2r with y = k z folded upstream).
+// -1/d for 1 <= d <= 2^126 + 1 on the FMA pipe: bit-trick seed (|rel err| <=
+// 5.1 %, the sign set by the wrapping subtraction; always a normal number in
+// this range), one cubic Newton step (1.3e-4), one quadratic step (~2e-8,
+// below half an fp32 ulp before rounding).  Negated so no FFMA2 operand
+// needs a negation.
+__device__ __forceinline__ float2 nrcp2_fma(float2 d) {
+  float2 s = make_float2(__uint_as_float(0xFEF311C3u - __float_as_uint(d.x)),
+                         __uint_as_float(0xFEF311C3u - __float_as_uint(d.y)));
+  const float2 one = make_float2(1.f, 1.f);
+  float2 e = __ffma2_rn(d, s, one);      // 1 - d/|d| (relative error of the seed)
+  const float2 q = __ffma2_rn(e, e, e);  // e + e^2
+  s = __ffma2_rn(s, q, s);               // s (1 + e + e^2)
+  e = __ffma2_rn(d, s, one);
+  return __ffma2_rn(s, e, s);
+}
+// s = -1 / (1 + 2^y) on a pair (tanh(z) = 1 + 2s with y = k z; the weights
+// are folded accordingly, tc_build_fragments).  The ex2 runs on the SFU; the
+// reciprocal on the SFU too unless SW, where it runs on the FMA pipe: at 4 SFU
+// lanes per scheduler a warp-wide MUFU holds the pipe 8 cycles, and two per
+// activation were the longest serial resource of a step.  SW clamps y at 126
+// first (2^y must stay finite for the Newton residual).
+template <bool SW = false>
 __device__ __forceinline__ float2 act_r2(float y0, float y1) {
-  const float2 d = __fadd2_rn(make_float2(tc_ex2(y0), tc_ex2(y1)), make_float2(1.f, 1.f));
-  return make_float2(tc_rcp(d.x), tc_rcp(d.y));
+  if constexpr (SW) {
+    const float2 d = __fadd2_rn(make_float2(tc_ex2(fminf(y0, 126.f)), tc_ex2(fminf(y1, 126.f))), make_float2(1.f, 1.f));
+    return nrcp2_fma(d);
+  } else {
+    const float2 d = __fadd2_rn(make_float2(tc_ex2(y0), tc_ex2(y1)), make_float2(1.f, 1.f));
+    return make_float2(tc_rcp(-d.x), tc_rcp(-d.y));
+  }
 }
 
+// Which of the four activation pairs of acc_to_a take the FMA-pipe
+// reciprocal (bit mask).  Measured (profiles/README.md): half at H = 32
+// balances the SFU against the issue slots (c0 -5 %, c1 -1 %, K = 262144
+// unchanged); at H = 64 the issue slots are the binding resource and the
+// SFU reciprocal is faster (all-FMA: +11 % at c2).
+template <int H>
+__host__ __device__ constexpr int tc_sw_rcp() {
+#ifdef MPPI_TC_SW_RCP
+  return MPPI_TC_SW_RCP;
+#else
+  return H == 32 ? 10 : 0;
+#endif
+}
 // Accumulator (n-tiles 2kk, 2kk+1) -> activation -> A fragment hi/lo of k-tile kk.
+template <int SW>  // bit i: pair i of the four uses the FMA-pipe reciprocal
 __device__ __forceinline__ void acc_to_a(const float (&d0)[4], const float (&d1)[4], uint32_t (&ahi)[4],
                                          uint32_t (&alo)[4]) {
-  const float2 r00 = act_r2(d0[0], d0[1]), r01 = act_r2(d0[2], d0[3]);
-  const float2 r10 = act_r2(d1[0], d1[1]), r11 = act_r2(d1[2], d1[3]);
+  const float2 r00 = act_r2<(SW & 1) != 0>(d0[0], d0[1]), r01 = act_r2<(SW & 2) != 0>(d0[2], d0[3]);
+  const float2 r10 = act_r2<(SW & 4) != 0>(d1[0], d1[1]), r11 = act_r2<(SW & 8) != 0>(d1[2], d1[3]);
   split2(r00.x, r00.y, ahi[0], alo[0]);  // row g,   k = 2t, 2t+1
   split2(r01.x, r01.y, ahi[1], alo[1]);  // row g+8, k = 2t, 2t+1
   split2(r10.x, r10.y, ahi[2], alo[2]);  // row g,   k = 2t+8, 2t+9
@@ -163,9 +211,16 @@ __device__ __forceinline__ void acc2_sum(const Acc2& a, float (&d)[4]) {
   d[3] = y.y;
 }
 
+// The layer-1 A operand in fragment order: plane hl (0 hi, 1 lo), word
+// tc_in_word(g, p, h) holds the fp16x2 input pair p of sample row g + 8h, so
+// lane (g, t) reads its {row g, row g+8} operand pair as one LDS.64 straight
+// into the HMMA source registers.  Pairs: (roll,vx), (vy,thd), (v0,v1), (1,0).
+// The pair index is XOR-swizzled by g >> 2 so the owners' 32-bit stores are
+// bank-conflict-free as well as the reads.
+__device__ __forceinline__ int tc_in_word(int g, int p, int h) { return g * 8 + 2 * (p ^ (g >> 2)) + h; }
 template <int MT>
 struct TcStage {
-  uint2 in[MT][16][4];     // per sample row: (hi, lo) of (roll,vx), (vy,thd), (v0,v1), (1,0)
+  uint32_t in[MT][2][64];  // [tile][hi/lo][tc_in_word]
   float4 out[MT][16];      // layer-3 outputs per sample row
 };
 constexpr int kTcTB = 16;  // timesteps per block of the numerator reduction
@@ -179,22 +234,24 @@ constexpr int kTcRedStride = 33;  // doubles per row (padding: conflict-free col
 template <int H, int MT, class B2Frag, class Side1, class Side2>
 __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, const uint32_t (&w1)[2 * (H / 8)],
                                        B2Frag&& b2frag, const uint32_t (&w3)[4 * (H / 16)],
-                                       const float (&b2)[2 * (H / 8)], const float (&b3)[2], float (&d3)[MT][4],
+                                       const float (&b2)[H / 8][4], const float (&b3)[4], float (&d3)[MT][4],
                                        Side1&& side1, Side2&& side2) {
   constexpr int NJ = H / 8, NK = H / 16;
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     // ---- layer 1 (k8): A rows g, g+8; k = 2t, 2t+1 (bias through the constant-one column)
-    const uint2 ag = st.in[m][g][t4], ag8 = st.in[m][g + 8][t4];
+    const int w = tc_in_word(g, t4, 0);
+    const uint2 ah = *reinterpret_cast<const uint2*>(&st.in[m][0][w]);  // hi: rows g, g+8
+    const uint2 al = *reinterpret_cast<const uint2*>(&st.in[m][1][w]);  // lo
     float d1[NJ][4];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       Acc2 a;
 #pragma unroll
       for (int i = 0; i < 4; ++i) a.m[i] = a.c[i] = 0.f;
-      mma_k8(a.c, ag.y, ag8.y, w1[2 * j]);      // lo * hi
-      mma_k8(a.c, ag.x, ag8.x, w1[2 * j + 1]);  // hi * lo
-      mma_k8(a.m, ag.x, ag8.x, w1[2 * j]);      // hi * hi
+      mma_k8(a.c, al.x, al.y, w1[2 * j]);      // lo * hi
+      mma_k8(a.c, ah.x, ah.y, w1[2 * j + 1]);  // hi * lo
+      mma_k8(a.m, ah.x, ah.y, w1[2 * j]);      // hi * hi
       acc2_sum(a, d1[j]);
     }
     if (m == MT - 1) side1();
@@ -202,21 +259,22 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
     Acc2 a2[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-      a2[j].m[0] = a2[j].m[2] = b2[2 * j];
-      a2[j].m[1] = a2[j].m[3] = b2[2 * j + 1];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a2[j].c[i] = 0.f;
     }
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
       uint32_t ahi[4], alo[4];
-      acc_to_a(d1[2 * kk], d1[2 * kk + 1], ahi, alo);
+      acc_to_a<tc_sw_rcp<H>()>(d1[2 * kk], d1[2 * kk + 1], ahi, alo);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const uint4 b = b2frag(kk, j);  // b0 hi, b0 lo, b1 hi, b1 lo
         mma_k16(a2[j].c, alo, b.x, b.z);
         mma_k16(a2[j].c, ahi, b.y, b.w);
-        mma_k16(a2[j].m, ahi, b.x, b.z);
+        if (kk == 0)
+          mma_k16_c(a2[j].m, ahi, b.x, b.z, b2[j]);  // the bias enters as C
+        else
+          mma_k16(a2[j].m, ahi, b.x, b.z);
       }
     }
     float d2[NJ][4];
@@ -225,18 +283,19 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
     if (m == MT - 1) side2();
     // ---- layer 3 (NK x k16, n = 8: outputs 0..3)
     Acc2 a3;
-    a3.m[0] = a3.m[2] = b3[0];
-    a3.m[1] = a3.m[3] = b3[1];
 #pragma unroll
     for (int i = 0; i < 4; ++i) a3.c[i] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
       uint32_t ahi[4], alo[4];
-      acc_to_a(d2[2 * kk], d2[2 * kk + 1], ahi, alo);
+      acc_to_a<tc_sw_rcp<H>()>(d2[2 * kk], d2[2 * kk + 1], ahi, alo);
       const int b = kk * 4;
       mma_k16(a3.c, alo, w3[b], w3[b + 2]);
       mma_k16(a3.c, ahi, w3[b + 1], w3[b + 3]);
-      mma_k16(a3.m, ahi, w3[b], w3[b + 2]);
+      if (kk == 0)
+        mma_k16_c(a3.m, ahi, w3[b], w3[b + 2], b3);
+      else
+        mma_k16(a3.m, ahi, w3[b], w3[b + 2]);
     }
     acc2_sum(a3, d3[m]);
   }
@@ -275,7 +334,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   using L = TcLayout<H>;
   uint32_t w1[2 * L::NJ], w3[4 * L::NK];
   uint32_t w2r[L::W2_SMEM ? 1 : 4 * L::NK * L::NJ];
-  float b2[2 * L::NJ], b3[2];
+  float b2[L::NJ][4], b3[4];  // bias quads in accumulator order {c, c+1, c, c+1}
   __shared__ __align__(16) uint4 s_w2[L::W2_SMEM ? L::NK * L::NJ : 1][32];
 #pragma unroll
   for (int i = 0; i < 2 * L::NJ; ++i) w1[i] = frag[(L::W1 + i) * 32 + lane];
@@ -289,10 +348,25 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   }
 #pragma unroll
   for (int i = 0; i < 4 * L::NK; ++i) w3[i] = frag[(L::W3 + i) * 32 + lane];
+  // each quad word is its own load (an opaque one for the repeats), so the
+  // compiler keeps four live registers instead of re-assembling the quad
+  // with moves every step
+  auto ld_opaque = [](const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return __uint_as_float(v);
+  };
 #pragma unroll
-  for (int i = 0; i < 2 * L::NJ; ++i) b2[i] = __uint_as_float(frag[(L::B2 + i) * 32 + lane]);
+  for (int j = 0; j < L::NJ; ++j) {
+    b2[j][0] = __uint_as_float(frag[(L::B2 + 2 * j) * 32 + lane]);
+    b2[j][1] = __uint_as_float(frag[(L::B2 + 2 * j + 1) * 32 + lane]);
+    b2[j][2] = ld_opaque(frag + (L::B2 + 2 * j) * 32 + lane);
+    b2[j][3] = ld_opaque(frag + (L::B2 + 2 * j + 1) * 32 + lane);
+  }
   b3[0] = __uint_as_float(frag[L::B3 * 32 + lane]);
   b3[1] = __uint_as_float(frag[(L::B3 + 1) * 32 + lane]);
+  b3[2] = ld_opaque(frag + L::B3 * 32 + lane);
+  b3[3] = ld_opaque(frag + (L::B3 + 1) * 32 + lane);
   auto b2frag = [&](int kk, int j) -> uint4 {
     if constexpr (L::W2_SMEM) {
       return s_w2[kk * L::NJ + j][lane];
@@ -304,7 +378,11 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
 
   TcStage<MT>& st = s_stage[warp];
   // the constant-one input column (k = 6: bias of layer 1), written once
-  for (int i = lane; i < CH; i += 32) st.in[i >> 4][i & 15][3] = make_uint2(h2_bits(__floats2half2_rn(1.f, 0.f)), 0u);
+  for (int i = lane; i < CH; i += 32) {
+    const int w = tc_in_word(i & 7, 3, (i >> 3) & 1);
+    st.in[i >> 4][0][w] = h2_bits(__floats2half2_rn(1.f, 0.f));
+    st.in[i >> 4][1][w] = 0u;
+  }
 
   // ---- owner: the sample this lane runs the scalar path for
   const int m_own = (MT == 2) ? (t4 >> 1) : 0;
@@ -391,17 +469,31 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // next pair is unconditional code in the odd step).
   auto step = [&](int t, auto even_tag) {
     constexpr bool EVEN = decltype(even_tag)::value;
+    // pose of x_{t+1}: the Euler split (dynamics.cpp:137-148) reads only the
+    // old state, so it runs before the MLP and the costmap taps of x_{t+1}
+    // are in flight for a whole step before its cost consumes them
+    float sn, cs;
+    tc_sincos(th, sn, cs);
+    px = add_rn(px, mul_rn(sub_rn(mul_rn(cs, vx), mul_rn(sn, vy)), dt));
+    py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx), mul_rn(cs, vy)), dt));
+    th = add_rn(th, mul_rn(thd, dt));
+    const MapTaps<float> q_next = map_fetch(map, px, py);
     // stage this step's inputs (owner; MT = 1 mirror lanes store the same
     // values to the same row, so no branch splits the step's basic block)
     {
-      uint2* row = st.in[m_own][row_own];
+      uint32_t* hi_plane = st.in[m_own][0];
+      uint32_t* lo_plane = st.in[m_own][1];
+      const int h = t4 & 1;
       uint32_t hi, lo;
       split2(roll, vx, hi, lo);
-      row[0] = make_uint2(hi, lo);
+      hi_plane[tc_in_word(g, 0, h)] = hi;
+      lo_plane[tc_in_word(g, 0, h)] = lo;
       split2(vy, thd, hi, lo);
-      row[1] = make_uint2(hi, lo);
+      hi_plane[tc_in_word(g, 1, h)] = hi;
+      lo_plane[tc_in_word(g, 1, h)] = lo;
       split2(v0c, v1c, hi, lo);
-      row[2] = make_uint2(hi, lo);
+      hi_plane[tc_in_word(g, 2, h)] = hi;
+      lo_plane[tc_in_word(g, 2, h)] = lo;
     }
     __syncwarp();
     float d3[MT][4];
@@ -425,18 +517,12 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     }
     __syncwarp();
     const float4 d = st.out[m_own][row_own];
-    // Euler split (dynamics.cpp:137-148) from the old state
-    float sn, cs;
-    tc_sincos(th, sn, cs);
-    const float vx_old = vx, vy_old = vy, thd_old = thd;
+    // the dynamic block of the Euler split
     roll = add_rn(roll, mul_rn(d.x, dt));
     vx = add_rn(vx, mul_rn(d.y, dt));
     vy = add_rn(vy, mul_rn(d.z, dt));
     thd = add_rn(thd, mul_rn(d.w, dt));
-    px = add_rn(px, mul_rn(sub_rn(mul_rn(cs, vx_old), mul_rn(sn, vy_old)), dt));
-    py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx_old), mul_rn(cs, vy_old)), dt));
-    th = add_rn(th, mul_rn(thd_old, dt));
-    q = map_fetch(map, px, py);  // consumed by the next step's cost
+    q = q_next;  // consumed by the next step's cost
     p_roll = roll;
     p_vx = vx;
     p_vy = vy;
