@@ -171,7 +171,10 @@ struct Handle final : HandleBase {
   }
   std::string variant_name() const override {
     char buf[160];
-    if (use_tc)
+    if (use_tc && tc_detail::g_tc_last_pair)
+      std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, merge + epilogue kernels)",
+                    H, cfg.noise_mode, n_chunks);
+    else if (use_tc)
       std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=%d,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %s)",
                     H, tc_mt, cfg.noise_mode, chunk_samples, n_chunks,
                     coop_tail() ? "cooperative merge+epilogue" : "merge + epilogue kernels");

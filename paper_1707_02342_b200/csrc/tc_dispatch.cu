@@ -9,6 +9,10 @@
 
 namespace mppi_host {
 
+namespace tc_detail {
+int g_tc_last_pair = 0;
+}
+
 template <int H>
 cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
                               const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,

@@ -3,6 +3,7 @@
 // tc_h32.cu / tc_h64.cu (define TC_H before including) so the variants build
 // in parallel.
 #include "rollout_tc.cuh"
+#include "rollout_tc_pair.cuh"
 #include "ws_launch.hpp"
 
 #include <algorithm>
@@ -49,6 +50,42 @@ cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
   }
   return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, tail, n_chunks, ctrls, smem, stream);
 }
+// The warp-pair kernel (rollout_tc_pair.cuh): H = 32, eps' on chip, no trace.
+// Used by default only at no more than one chunk per SM (c0: K1 -5 %); with
+// more chunks per SM its barrier handoffs cost more than the shorter per-warp
+// chain saves (c1: +24 %, profiles/README.md).  MPPI_TC_PAIR=1 forces it (when
+// its grid is resident at once), MPPI_TC_PAIR=0 disables it.
+constexpr int kTcPairs = 1;  // warp pairs (chunks) per CTA
+template <int Mode, bool STAB>
+bool pair_fits(int T, int n_chunks, int ctrls) {
+  const char* e = std::getenv("MPPI_TC_PAIR");
+  if (e && std::atoi(e) == 0) return false;
+  auto kern = mppi_dev::rollout_tc_pair_kernel<kTcPairs, Mode, STAB>;
+  const size_t smem = mppi_dev::tc_pair_smem_bytes(T, kTcPairs);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64 * kTcPairs, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const long long ctas = static_cast<long long>((n_chunks + kTcPairs - 1) / kTcPairs) * ctrls;
+  if (!(e && std::atoi(e) == 1) && static_cast<long long>(n_chunks) * ctrls > sms) return false;
+  return ctas <= static_cast<long long>(per_sm) * sms;
+}
+template <int Mode, bool STAB>
+cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
+                    cudaStream_t stream) {
+  auto kern = mppi_dev::rollout_tc_pair_kernel<kTcPairs, Mode, STAB>;
+  const size_t smem = mppi_dev::tc_pair_smem_bytes(a.T, kTcPairs);
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const dim3 grid((n_chunks + kTcPairs - 1) / kTcPairs, ctrls);
+  g_tc_last_pair = 1;
+  kern<<<grid, 64 * kTcPairs, smem, stream>>>(a, frag);
+  return cudaGetLastError();
+}
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (2 CTAs of 4 warps per SM); larger launches regenerate it from the counters.
 template <int H, int MT, int Mode, bool STAB>
@@ -67,6 +104,11 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, cons
   const long long ctas = static_cast<long long>((n_chunks + kTcWarps - 1) / kTcWarps) * ctrls;
   const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
                                                    : (base + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
+  g_tc_last_pair = 0;
+  if constexpr (H == 32 && MT == 1) {
+    if (!a.trace_states && tail.mode == 0 && pair_fits<Mode, STAB>(a.T, n_chunks, ctrls))
+      return go_pair<Mode, STAB>(a, frag, n_chunks, ctrls, stream);
+  }
   // (MT = 2 serves K > 32768, whose grid never fits one wave: no on-chip eps')
   if constexpr (MT == 1) {
     if (store && !a.trace_states)

@@ -18,6 +18,8 @@ cudaError_t launch_rollout_ws_h64(const mppi_dev::RolloutArgs<float>& a, const m
                                   int mode, int L, bool smem_weights, dim3 grid, size_t smem, cudaStream_t stream);
 
 namespace tc_detail {
+// whether the last tensor-core K1 enqueued was the warp-pair kernel (reporting)
+extern int g_tc_last_pair;
 // the per-(H, noise mode) launchers, one translation unit each (tc_h*_*.cu)
 template <int H, int Mode>
 cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,

@@ -351,7 +351,7 @@ def test_kernel_variant_and_launch_count():
     n0 = g.launch_count
     g.mpc_step(w.x0[0])
     # the fp32 H = 32 vehicle path is the tensor-core K1 (+ the epilogue kernel)
-    assert "rollout_tc_kernel" in g.kernel_variant
+    assert "rollout_tc_pair_kernel" in g.kernel_variant  # one wave at this size: the warp-pair K1
     assert g.launch_count - n0 in (1, 2)  # cooperative K1, or K1 + tail kernel (merge + epilogue)
     w64 = workload.make("c2", samples=256, horizon_steps=20)
     g64, _ = pair(w64, "fp32", "philox")
@@ -398,3 +398,47 @@ def test_tail_styles_agree(K):
     assert res["coop"]["launches"] == 3 and res["kernels"]["launches"] == 6
     assert res["coop"]["plan"] == res["kernels"]["plan"] and res["coop"]["u"] == res["kernels"]["u"]
     assert all(r["it"] == 3 for r in res.values())
+
+
+_PAIR_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+from paper_1707_02342_b200 import workload
+from paper_1707_02342_b200.api import Controller, CostParams
+K, T, noise, form = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
+w = workload.make('c1', samples=K, horizon_steps=T)
+cost = CostParams() if form == 'reference' else w.cost
+g = Controller(w.params, w.bounds, w.sg, cost, hidden=32, precision='fp32', noise=noise)
+g.set_mlp(w.mlp); g.set_costmap(w.costmap)
+g.plan = np.random.default_rng(3).uniform(-0.4, 0.4, (T, 2))
+costs = g.rollout_batch(w.x0[0])
+u = [g.mpc_step(w.x0[0]).tolist() for _ in range(3)]
+print(json.dumps({'costs': costs.tolist(), 'plan': g.plan.tolist(), 'u': u, 'variant': g.kernel_variant}))
+"""
+
+
+@pytest.mark.parametrize("K,T,noise,form", [(1920, 100, "philox", "baseline"), (16384, 100, "philox", "baseline"),
+                                            (1000, 37, "philox", "reference"), (500, 20, "ref_splitmix", "baseline")])
+def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
+    """The warp-pair K1 (one chunk per two warps, hidden units and scalar work
+    split between them; rollout_tc_pair.cuh) performs exactly the single-warp
+    tensor-core kernel's operations: costs, plans and controls are
+    bit-identical (odd T, a ragged last chunk, the side-slip cost term and the
+    reference noise stream included)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):  # MPPI_TC_PAIR=0 / 1 force the single-warp / the pair kernel
+        env = dict(os.environ, MPPI_TC_PAIR=flag)
+        out = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(K), str(T), noise, form], env=env,
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[flag] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert "rollout_tc_pair_kernel" in res["1"]["variant"], res["1"]["variant"]
+    assert "rollout_tc_kernel" in res["0"]["variant"], res["0"]["variant"]
+    assert res["0"]["costs"] == res["1"]["costs"]
+    assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
