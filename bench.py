@@ -235,7 +235,14 @@ def run_ours(args):
         ms = ctrl.closed_loop_timed(x0, args.steps, L2_FLUSH_BYTES)
     barrier()
     launches = ctrl.launch_count - n_launch0
+    # K1's own launch duration (roofline): a separate pass of the iteration
+    # graph that brackets K1 with event nodes (not in the timed region: those
+    # nodes would cut the tail's programmatic-launch edge to K1)
+    ctrl.profile(True)
+    ctrl.profile_read(reset=True)
+    ctrl.closed_loop_timed(x0, min(args.steps, 50), L2_FLUSH_BYTES)
     k1_ms, k1_n = ctrl.profile_read(reset=True)
+    ctrl.profile(False)
     t = torch.tensor([ms, k1_ms / max(k1_n, 1)], dtype=torch.float64, device="cuda")
     if pg:
         pg.all_reduce(t, op=pg.ReduceOp.MAX)

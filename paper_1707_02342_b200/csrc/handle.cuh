@@ -209,7 +209,7 @@ struct Handle final : HandleBase {
   DevBuf<unsigned> d_tail_cnt;
   DevBuf<unsigned char> d_plantw;  // MlpParams<float, H> (the plant step of the tail)
   int coop_state = 0;  // 1: the cooperative K1 fits (one controller, one wave)
-  int graph_kernels[3] = {0, 0, 0};
+  int graph_kernels[4] = {0, 0, 0, 0};
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   int rank = 0, world = 1;
   int zero_start = 0;
@@ -257,9 +257,9 @@ struct Handle final : HandleBase {
   uint64_t prof_launches = 0;
 
   // graphs: 0 = step (compute+slide), 1 = compute only, 2 = closed-loop iteration
-  cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t n_before_capture = 0;
-  bool graph_trace[3] = {false, false, false};
+  bool graph_trace[4] = {false, false, false, false};
 
   explicit Handle(const mppi_gpu_config& c) : cfg(c) {
     validate_config(c);
@@ -945,7 +945,7 @@ struct Handle final : HandleBase {
       cudaGraph_t g = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       try {
-        if (which != 2) {
+        if (which < 2) {
           CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
           CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
         }
@@ -954,7 +954,7 @@ struct Handle final : HandleBase {
         n_before_capture = launches;
         enqueue_iteration(cfg.noise_mode, /*events=*/which == 2, slide, /*increment=*/slide, plant, trace);
         profile = prof;
-        if (which != 2)
+        if (which < 2)
           CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
       } catch (...) {
         cudaStreamEndCapture(stream, &g);
@@ -1045,10 +1045,11 @@ struct Handle final : HandleBase {
       d_xtrace.alloc(static_cast<size_t>(iterations + 1) * C * 8);
       CUDA_TRY(cudaMemcpyAsync(d_xtrace.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
       // graphs hold trace pointers: re-capture if the buffers moved
-      if (graph[2]) {
-        cudaGraphExecDestroy(graph[2]);
-        graph[2] = nullptr;
-      }
+      for (int w = 2; w < 4; ++w)
+        if (graph[w]) {
+          cudaGraphExecDestroy(graph[w]);
+          graph[w] = nullptr;
+        }
     }
     if (flush_bytes) d_flush.alloc(flush_bytes);
     CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
@@ -1057,21 +1058,26 @@ struct Handle final : HandleBase {
     double total = 0.0;
     const bool per_iter_timing = flush_bytes > 0;
     if (!per_iter_timing && ms_out) CUDA_TRY(cudaEventRecord(ev_it0, stream));
+    // The iteration graph without event nodes (slot 3): an event record node
+    // between K1 and the tail would cut the tail's programmatic (PDL) edge to
+    // K1.  With profiling on (set_profile), the graph that brackets K1 with
+    // event nodes (slot 2) runs instead and K1's own durations (the roofline's
+    // denominator) accumulate for read_profile.
+    const bool k1_events = profile;
     for (int i = 0; i < iterations; ++i) {
       if (per_iter_timing) {
         CUDA_TRY(cudaMemsetAsync(d_flush.p, i & 0xff, flush_bytes, stream));
         CUDA_TRY(cudaEventRecord(ev_it0, stream));
       }
-      run_graph(2, true, true, trace);
+      run_graph(k1_events ? 2 : 3, true, true, trace);
       if (per_iter_timing) {
         CUDA_TRY(cudaEventRecord(ev_it1, stream));
         CUDA_TRY(cudaEventSynchronize(ev_it1));
         float ms = 0;
         CUDA_TRY(cudaEventElapsedTime(&ms, ev_it0, ev_it1));
         total += ms;
-        // rollout-kernel share, from the event nodes captured around K1
         float k1 = 0;
-        if (cudaEventElapsedTime(&k1, ev_a, ev_b) == cudaSuccess) {
+        if (k1_events && cudaEventElapsedTime(&k1, ev_a, ev_b) == cudaSuccess) {
           prof_ms += k1;
           ++prof_launches;
         } else {

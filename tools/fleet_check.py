@@ -21,7 +21,11 @@ def run(C, K, perturb, steps=10):
     c.closed_loop_timed(x, 3, 256 << 20)
     c.profile_read(reset=True)
     ms = c.closed_loop_timed(x, steps, 256 << 20)
+    c.profile(True)  # K1 durations: the event-bracketed graph, a separate pass
+    c.profile_read(reset=True)
+    c.closed_loop_timed(x, min(steps, 30), 256 << 20)
     k1, n = c.profile_read(reset=True)
+    c.profile(False)
     u, xt = c.closed_loop(x, 2, traces=True)
     print(json.dumps({"C": C, "K": K, "perturb": perturb, "ms_per_iter": ms / steps, "k1_ms": k1 / max(n, 1),
                       "Gsteps_per_s": C * K * 100 / (ms / steps * 1e-3) / 1e9, "kernel": c.kernel_variant,
