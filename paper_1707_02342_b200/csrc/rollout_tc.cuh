@@ -77,6 +77,15 @@ __device__ __forceinline__ void mma_k16_c(float (&d)[4], const uint32_t (&a)[4],
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]), "f"(c[3]));
 }
 
+// A load the compiler cannot merge with an identical one: the repeated words
+// of the bias quads {c, c+1, c, c+1} then stay in four live registers instead
+// of being re-assembled with moves every step.
+__device__ __forceinline__ float tc_ld_opaque(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return __uint_as_float(v);
+}
+
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 // (x, y) -> fp16x2 hi and lo words: hi = fp16(x), lo = fp16(x - hi).
@@ -218,6 +227,21 @@ __device__ __forceinline__ void acc2_sum(const Acc2& a, float (&d)[4]) {
 // The pair index is XOR-swizzled by g >> 2 so the owners' 32-bit stores are
 // bank-conflict-free as well as the reads.
 __device__ __forceinline__ int tc_in_word(int g, int p, int h) { return g * 8 + 2 * (p ^ (g >> 2)) + h; }
+// c = sum of the per-k-tile cross-term accumulators, in k-tile order
+template <int NK>
+__device__ __forceinline__ void tc_sum_cross(const float (&c)[NK][4], float (&out)[4]) {
+  float2 x = make_float2(c[0][0], c[0][1]), y = make_float2(c[0][2], c[0][3]);
+#pragma unroll
+  for (int kk = 1; kk < NK; ++kk) {
+    x = __fadd2_rn(x, make_float2(c[kk][0], c[kk][1]));
+    y = __fadd2_rn(y, make_float2(c[kk][2], c[kk][3]));
+  }
+  out[0] = x.x;
+  out[1] = x.y;
+  out[2] = y.x;
+  out[3] = y.y;
+}
+
 template <int MT>
 struct TcStage {
   uint32_t in[MT][2][64];  // [tile][hi/lo][tc_in_word]
@@ -282,21 +306,27 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
     for (int j = 0; j < NJ; ++j) acc2_sum(a2[j], d2[j]);
     if (m == MT - 1) side2();
     // ---- layer 3 (NK x k16, n = 8: outputs 0..3)
+    // (the last layer ends the step's dependent chain: its cross terms
+    // accumulate per k-tile, two chains of two instead of one of 2*NK)
     Acc2 a3;
+    float c3[NK][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a3.c[i] = 0.f;
+    for (int kk = 0; kk < NK; ++kk)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c3[kk][i] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
       uint32_t ahi[4], alo[4];
       acc_to_a<tc_sw_rcp<H>()>(d2[2 * kk], d2[2 * kk + 1], ahi, alo);
       const int b = kk * 4;
-      mma_k16(a3.c, alo, w3[b], w3[b + 2]);
-      mma_k16(a3.c, ahi, w3[b + 1], w3[b + 3]);
+      mma_k16(c3[kk], alo, w3[b], w3[b + 2]);
+      mma_k16(c3[kk], ahi, w3[b + 1], w3[b + 3]);
       if (kk == 0)
         mma_k16_c(a3.m, ahi, w3[b], w3[b + 2], b3);
       else
         mma_k16(a3.m, ahi, w3[b], w3[b + 2]);
     }
+    tc_sum_cross<NK>(c3, a3.c);
     acc2_sum(a3, d3[m]);
   }
 }
@@ -348,25 +378,17 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   }
 #pragma unroll
   for (int i = 0; i < 4 * L::NK; ++i) w3[i] = frag[(L::W3 + i) * 32 + lane];
-  // each quad word is its own load (an opaque one for the repeats), so the
-  // compiler keeps four live registers instead of re-assembling the quad
-  // with moves every step
-  auto ld_opaque = [](const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
-    return __uint_as_float(v);
-  };
 #pragma unroll
   for (int j = 0; j < L::NJ; ++j) {
     b2[j][0] = __uint_as_float(frag[(L::B2 + 2 * j) * 32 + lane]);
     b2[j][1] = __uint_as_float(frag[(L::B2 + 2 * j + 1) * 32 + lane]);
-    b2[j][2] = ld_opaque(frag + (L::B2 + 2 * j) * 32 + lane);
-    b2[j][3] = ld_opaque(frag + (L::B2 + 2 * j + 1) * 32 + lane);
+    b2[j][2] = tc_ld_opaque(frag + (L::B2 + 2 * j) * 32 + lane);
+    b2[j][3] = tc_ld_opaque(frag + (L::B2 + 2 * j + 1) * 32 + lane);
   }
   b3[0] = __uint_as_float(frag[L::B3 * 32 + lane]);
   b3[1] = __uint_as_float(frag[(L::B3 + 1) * 32 + lane]);
-  b3[2] = ld_opaque(frag + L::B3 * 32 + lane);
-  b3[3] = ld_opaque(frag + (L::B3 + 1) * 32 + lane);
+  b3[2] = tc_ld_opaque(frag + L::B3 * 32 + lane);
+  b3[3] = tc_ld_opaque(frag + (L::B3 + 1) * 32 + lane);
   auto b2frag = [&](int kk, int j) -> uint4 {
     if constexpr (L::W2_SMEM) {
       return s_w2[kk * L::NJ + j][lane];

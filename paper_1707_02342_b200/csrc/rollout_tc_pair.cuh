@@ -34,12 +34,6 @@ struct TcPairStage {
 
 __device__ __forceinline__ void tc_pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-__device__ __forceinline__ float tc_ld_opaque(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
-  return __uint_as_float(v);
-}
-
 // grid = (ceil(chunks / NP), controllers), block = 64 * NP (NP pairs).
 // Dynamic smem: plan (2T + 2 floats), then eps' [NP][T][16] float2 and the
 // coupling terms [NP][T][16] float (tc_pair_smem_bytes).
@@ -282,20 +276,22 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
     if (half == 0) {
       // ---- layer 3 (k-tile 0 own, k-tile 1 from the control warp; as tc_mlp)
       Acc2 a3;
+      float c3[2][4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a3.c[i] = 0.f;
+      for (int i = 0; i < 4; ++i) c3[0][i] = c3[1][i] = 0.f;
       uint32_t phi[4], plo[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         phi[i] = st.xa[1][1][i][lane];
         plo[i] = st.xa[1][1][4 + i][lane];
       }
-      mma_k16(a3.c, alo, w3[0], w3[2]);
-      mma_k16(a3.c, ahi, w3[1], w3[3]);
+      mma_k16(c3[0], alo, w3[0], w3[2]);
+      mma_k16(c3[0], ahi, w3[1], w3[3]);
       mma_k16_c(a3.m, ahi, w3[0], w3[2], b3);
-      mma_k16(a3.c, plo, w3[4], w3[6]);
-      mma_k16(a3.c, phi, w3[5], w3[7]);
+      mma_k16(c3[1], plo, w3[4], w3[6]);
+      mma_k16(c3[1], phi, w3[5], w3[7]);
       mma_k16(a3.m, phi, w3[4], w3[6]);
+      tc_sum_cross<2>(c3, a3.c);
       float d3[4];
       acc2_sum(a3, d3);
       if (t4 < 2) {

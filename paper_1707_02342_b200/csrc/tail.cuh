@@ -315,9 +315,12 @@ __global__ void __launch_bounds__(kMergeBlock) tail_kernel(const Acc* __restrict
   Acc* row = merged + static_cast<size_t>(ctrl) * stride;
   merge_elements<kMergeBlock>(partials + static_cast<size_t>(ctrl) * ctrl_stride, n, stride, lambda, row, blockIdx.x,
                               gridDim.x, reinterpret_cast<double*>(smem_raw));
-  __threadfence();
+  // merge_elements' writes are thread 0's: its fence orders them before the ticket
   __syncthreads();
-  if (threadIdx.x == 0) s_ticket = atomicAdd(counters + ctrl, 1u);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_ticket = atomicAdd(counters + ctrl, 1u);
+  }
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return;
   __threadfence();
