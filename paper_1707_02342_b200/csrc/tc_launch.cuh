@@ -150,7 +150,21 @@ cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, lon
   // programmatic dependent launch: the tail may launch before the previous
   // kernel (K1 or the pre-merge) ends and waits for it on the device
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::min(stride, 296), ctrls);
+  // After a one-wave K1 (at most 2 CTAs of 4 chunks per SM) the tail's CTAs
+  // launch early (PDL) only where K1 left room: a quarter-size grid (4
+  // elements per CTA) is resident before K1 ends and merges as fast (c1:
+  // -5 us per iteration; profiles/README.md).  Multi-wave K1s keep one
+  // element per CTA.
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  int grid = std::min(stride, 296);
+  if (n <= 8 * sms) grid = (stride + 3) / 4;
+  if (const char* g = std::getenv("MPPI_TAIL_GRID")) grid = std::max(1, std::min(std::min(stride, 296), std::atoi(g)));
+  cfg.gridDim = dim3(grid, ctrls);
   cfg.blockDim = dim3(mppi_dev::kMergeBlock);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
