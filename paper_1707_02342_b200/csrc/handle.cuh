@@ -387,9 +387,12 @@ struct Handle final : HandleBase {
     n_merged = n_chunks;
     // pre-merge groups of up to 32 chunks (each staged in shared memory,
     // <= ~160 KB) whenever the epilogue would otherwise walk > 2 tiles
-    // (tensor-core path: its element-parallel tail stages one scale per row in
-    // shared memory, so only very large launches pre-merge)
-    if ((!use_tc && n_chunks > 64) || (use_tc && n_chunks > 8192)) {
+    // (tensor-core path: above 1024 chunks, where the element-parallel tail's
+    // per-thread row walk outgrows the extra launch: c2 -27 us, K=262144
+    // -57 us per iteration; at c1's 1024 it does not pay)
+    int tc_min = 1024;
+    if (const char* e = std::getenv("MPPI_PREMERGE_MIN")) tc_min = std::atoi(e);
+    if ((!use_tc && n_chunks > 64) || (use_tc && n_chunks > tc_min)) {
       merge_G = std::max(1, std::min(32, static_cast<int>((160 * 1024) / (8 * partial_stride))));
       n_merged = (n_chunks + merge_G - 1) / merge_G;
       d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);

@@ -442,3 +442,23 @@ def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
     assert "rollout_tc_kernel" in res["0"]["variant"], res["0"]["variant"]
     assert res["0"]["costs"] == res["1"]["costs"]
     assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
+
+
+def test_tail_grid_does_not_change_results():
+    """Each merged element is summed by one CTA in a fixed row order, so the
+    tail's grid size (one element per CTA, or the quarter-size grid used after
+    a one-wave K1) cannot change a bit of the plan."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for grid in ("296", "51", "7"):
+        env = dict(os.environ, MPPI_TAIL_GRID=grid)
+        out = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, "16384"], env=env, capture_output=True,
+                             text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[grid] = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["296"]["plan"] == res["51"]["plan"] == res["7"]["plan"]
+    assert res["296"]["u"] == res["51"]["u"] == res["7"]["u"]
