@@ -316,6 +316,12 @@ class Controller:
         h = ctypes.c_void_p()
         check(self._lib.mppi_gpu_create(ctypes.byref(self.config), ctypes.byref(h)))
         self._h = h
+        # per-call host buffers of the hot path (mpc_step / compute_control),
+        # allocated once with their ctypes pointers: the per-step host cost is
+        # then one copy in, the C call and one copy out
+        self._xbuf = np.zeros(self.n_controllers * self.state_dim)
+        self._ubuf = np.zeros((self.n_controllers, 2))
+        self._xptr, self._uptr = dptr(self._xbuf), dptr(self._ubuf)
 
     # -- lifetime -----------------------------------------------------------
     def close(self) -> None:
@@ -398,16 +404,22 @@ class Controller:
         return x
 
     # -- hot path -----------------------------------------------------------
+    def _stage_x(self, x0) -> None:
+        x = np.asarray(x0, dtype=np.float64)
+        if x.size != self._xbuf.size:
+            raise InvalidArgument(_lib.MPPI_ERR_INVALID_ARGUMENT, "x0 dimension mismatch")
+        self._xbuf[:] = x.reshape(-1)
+
     def mpc_step(self, x0) -> np.ndarray:
         """mpc_step (controller.cpp:133-148): returns clamp(U'[0]) and slides."""
-        u = np.zeros((self.n_controllers, 2))
-        check(self._lib.mppi_gpu_step(self._h, dptr(self._x(x0)), dptr(u)))
-        return u[0] if self.n_controllers == 1 else u
+        self._stage_x(x0)
+        check(self._lib.mppi_gpu_step(self._h, self._xptr, self._uptr))
+        return self._ubuf[0].copy() if self.n_controllers == 1 else self._ubuf.copy()
 
     def compute_control(self, x0) -> np.ndarray:
-        u = np.zeros((self.n_controllers, 2))
-        check(self._lib.mppi_gpu_compute_control(self._h, dptr(self._x(x0)), dptr(u)))
-        return u[0] if self.n_controllers == 1 else u
+        self._stage_x(x0)
+        check(self._lib.mppi_gpu_compute_control(self._h, self._xptr, self._uptr))
+        return self._ubuf[0].copy() if self.n_controllers == 1 else self._ubuf.copy()
 
     def slide(self) -> None:
         check(self._lib.mppi_gpu_slide(self._h))
