@@ -40,6 +40,7 @@ struct EpilogueArgs {
   R* x0;                 // [C][8] (plant mode: advanced in place)
   uint64_t* iters;       // [C]
   StepStatus* status;    // [C]
+  StepStatus* status_host;  // [C] mapped pinned host mirror written directly (tensor-core tail), or nullptr
   R* u_trace;            // [iter][C][2] or nullptr
   R* x_trace;            // [iter+1][C][8] or nullptr
   const uint64_t* trace_base;  // [C] iteration at trace start

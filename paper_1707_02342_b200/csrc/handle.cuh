@@ -211,6 +211,7 @@ struct Handle final : HandleBase {
   int coop_state = 0;  // 1: the cooperative K1 fits (one controller, one wave)
   int graph_kernels[4] = {0, 0, 0, 0};
   int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
+  bool status_direct = false;      // capture in progress: the tail writes h_status itself
   int rank = 0, world = 1;
   int zero_start = 0;
   int partial_stride = 0;
@@ -852,6 +853,7 @@ struct Handle final : HandleBase {
         TailArgs ta{};
         ta.plant_w = d_plantw.p;
         ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
+        if (status_direct) ta.e.status_host = h_status.p;  // mapped pinned (UVA)
         enqueue_premerge();
         const Acc* rows = merge_G ? d_partials2.p : d_partials.p;
         const int n_rows = merge_G ? n_merged : n_chunks;
@@ -948,18 +950,26 @@ struct Handle final : HandleBase {
       cudaGraph_t g = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       try {
-        if (which < 2) {
-          CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
-          CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
-        }
+        // step graphs (slots 0, 1): x0 host-to-device, then K1.  The status
+        // is clear between steps (throw_status clears it after a failure), so
+        // no memset node.  (Reading x0 from the mapped host buffer in K1
+        // instead of this copy measured 17 us slower: every warp's PCIe read.)
+        if (which < 2) CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
         const bool prof = profile;
         profile = false;
         n_before_capture = launches;
+        // step graphs on the tensor-core path: the tail writes the host status
+        // mirror itself (no device-to-host copy node at the end of the graph)
+        status_direct = which < 2 && use_tc && !coop_tail() && std::is_same<R, float>::value &&
+                        cfg.weight_rule != MPPI_WEIGHT_CEM;
         enqueue_iteration(cfg.noise_mode, /*events=*/which == 2, slide, /*increment=*/slide, plant, trace);
         profile = prof;
-        if (which < 2)
+        const bool direct = status_direct;
+        status_direct = false;
+        if (which < 2 && !direct)
           CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
       } catch (...) {
+        status_direct = false;
         cudaStreamEndCapture(stream, &g);
         if (g) cudaGraphDestroy(g);
         throw;
@@ -985,6 +995,10 @@ struct Handle final : HandleBase {
     return code;
   }
   [[noreturn]] void throw_status(int code) {
+    // a failed step leaves the device status sticky (K1 aborts on it); clear
+    // it so the next call starts clean (the step graphs carry no memset)
+    cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream);
+    cudaStreamSynchronize(stream);
     if (code == MPPI_ERR_NONFINITE) throw Error(code, "it_weights: non-finite cost");
     if (code == MPPI_ERR_INVALID_ARGUMENT)
       throw Error(code, "ControlPlan: needs a finite T x m matrix, T >= 1");

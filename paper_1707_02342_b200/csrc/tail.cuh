@@ -168,6 +168,21 @@ __device__ __forceinline__ void tail_prefetch(const EpilogueArgs<float>& a, cons
       dst[i] = src[i];
   }
 }
+// The finished status of controller ctrl into the mapped host mirror (one
+// thread; its own earlier writes to *st are ordered before these reads): the
+// step graph then needs no device-to-host copy node.
+__device__ __forceinline__ void publish_status(const EpilogueArgs<float>& a, int ctrl) {
+  if (!a.status_host) return;
+  const StepStatus* st = a.status + ctrl;
+  StepStatus* sh = a.status_host + ctrl;
+  sh->code = st->code;
+  sh->u0[0] = st->u0[0];
+  sh->u0[1] = st->u0[1];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sh->x[i] = st->x[i];
+  sh->iteration = st->iteration;
+}
+
 template <int H>
 __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* row, int ctrl,
                                               unsigned char* smem, const unsigned char* pre) {
@@ -195,7 +210,10 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
     s_agg[i] = __ldcg(row + kPartialHeader + i) / eta_l;  // agg = num / eta, once per element
   __syncthreads();
   if (s_code != 0) {
-    if (threadIdx.x == 0 && __ldcg(&st->code) == 0) st->code = s_code;
+    if (threadIdx.x == 0) {
+      if (__ldcg(&st->code) == 0) st->code = s_code;
+      publish_status(a, ctrl);
+    }
     return;
   }
   // ---- SG smoothing of agg, U' = U + SG(agg)
@@ -222,7 +240,10 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
     s_new[i] = nv;
   }
   if (__syncthreads_or(nonfinite)) {  // ControlPlan rejects non-finite plans
-    if (threadIdx.x == 0) st->code = 1;
+    if (threadIdx.x == 0) {
+      st->code = 1;
+      publish_status(a, ctrl);
+    }
     return;
   }
   const float u0 = clamp_r(s_new[0], a.lo0, a.hi0), u1 = clamp_r(s_new[1], a.lo1, a.hi1);
@@ -291,6 +312,7 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   if (lane == 0) {
     a.iters[ctrl] = it;
     st->iteration = it;
+    publish_status(a, ctrl);
   }
 }
 
