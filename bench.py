@@ -285,7 +285,7 @@ def run_ours(args):
         e_ms = float(e_ms[0])
         e2e = {"value": units_per_step * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
                "h2d_bytes_per_step": C * 8 * 4, "d2h_bytes_per_step": C * 96,
-               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H"}
+               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H (written to pinned host memory by the tail kernel)"}
 
     if rank != 0:
         if pg:
