@@ -584,6 +584,26 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // blocks of kTcTB steps, products staged [t][c][lane] in shared memory and
   // summed per (t, c) over the lanes in ascending lane order by one lane each.
   double* red = s_red_all + static_cast<size_t>(warp) * (2 * kTcTB) * kTcRedStride;
+  if constexpr (STORE && MT == 1) {
+    // eps' is on chip: each lane sums whole (t, c) elements over the chunk's
+    // rows, in the lane order of the staged reduction below (row g, then row
+    // g + 8; the mirror lanes only add zeros there), so the partials are
+    // bit-identical to it and to the warp-pair kernel's
+    if (!dup) red[row_own] = wk;
+    __syncwarp();
+    for (int e = lane; e < 2 * T; e += 32) {
+      const int tt = e >> 1, c = e & 1;
+      Acc s = 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const float2 ea = s_eps[tt * CH + r], eb = s_eps[tt * CH + r + 8];
+        s = s + red[r] * static_cast<Acc>(c ? ea.y : ea.x);
+        s = s + red[r + 8] * static_cast<Acc>(c ? eb.y : eb.x);
+      }
+      if (active) out[kPartialHeader + e] = s;
+    }
+    __syncwarp();
+  } else {
   if constexpr (Mode != kPhilox) ns = make_noise<float, Mode>(a, ctrl, kn);
   for (int tb = 0; tb < T; tb += kTcTB) {
 #pragma unroll 2
@@ -611,6 +631,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     for (int l = 0; l < 32; ++l) s = s + col[l];
     if (active && tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
     __syncwarp();
+  }
   }
   // group merge / fused epilogue (tail.cuh); the reduction buffer is scratch now
   // cooperative tail (one controller, grid co-resident): merge of the chunk
