@@ -625,10 +625,16 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
       red[(2 * j + 1) * kTcRedStride + lane] = wk * static_cast<Acc>(e1);
     }
     __syncwarp();
-    Acc s = 0.0;
+    // four interleaved partial sums (lanes l = 4i + q), then q = 0..3: a
+    // fixed order with an 8-deep dependent chain instead of 32
+    Acc s4[4] = {0.0, 0.0, 0.0, 0.0};
     const double* col = red + lane * kTcRedStride;
-#pragma unroll 8
-    for (int l = 0; l < 32; ++l) s = s + col[l];
+#pragma unroll
+    for (int l = 0; l < 32; l += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s4[q] = s4[q] + col[l + q];
+    }
+    const Acc s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     if (active && tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
     __syncwarp();
   }
