@@ -644,8 +644,8 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // partials by all CTAs, then the epilogue by CTA 0 (tail.cuh)
   if (tail.mode == 1) {
     cooperative_groups::this_grid().sync();
-    merge_elements<32 * NW>(a.partials, a.chunk_end, a.partial_stride, a.dlambda, tail.merged, blockIdx.x, gridDim.x,
-                            s_red_all);
+    merge_elements<32 * NW, false>(a.partials, a.chunk_end, a.partial_stride, a.dlambda, tail.merged, blockIdx.x,
+                                   gridDim.x, s_red_all);
     cooperative_groups::this_grid().sync();
     if (blockIdx.x == 0)
       epilogue_body<float, H, VehicleMlp<float, H>, 32 * NW>(

@@ -27,6 +27,8 @@ namespace mppi_dev {
 
 constexpr int kMergeBlock = 128;
 constexpr int kMergeElems = 8;  // elements per pass of a CTA (independent loads in flight)
+constexpr int kMergeRows = 8;   // rows per thread of merge_elements' single-pass path
+constexpr int kMergeFastElems = 4;  // elements per CTA of that path (the tail's quarter-size grid)
 
 struct TailArgs {
   int mode;                             // 0: chunk partials only; 1: cooperative merge + epilogue in K1
@@ -58,11 +60,71 @@ __device__ __forceinline__ void block_sum_n(Acc (&v)[kMergeElems], Acc* s_part) 
 // One CTA (BLOCK threads): merged elements e0, e0 + estep, ... of the rows
 // P[0..n) (stride doubles each).  smem: merge_smem_bytes(n).  The CTA with
 // e0 == 0 also writes rho, bad and the reserved slot.
-template <int BLOCK>
+template <int BLOCK, bool FAST = true>
 __device__ void merge_elements(const Acc* P, int n, int stride, double lambda, Acc* merged, int e0, int estep,
                                double* smem) {
   double* s_scale = smem;
   double* s_part = smem + n;
+  // one pass over the rows when every thread holds at most kMergeRows of them
+  // and the CTA has at most kMergeFastElems elements: the element values
+  // are loaded together with rho (one round trip less) and the scales stay in
+  // registers.  Same per-thread row order and the same scale values as the
+  // general path below, so the sums are bit-identical.
+  // (FAST = false inside K1's cooperative tail: its registers would spill K1)
+  if (FAST && n <= kMergeRows * BLOCK && e0 + kMergeFastElems * estep >= stride) {
+    Acc rr[kMergeRows], x[kMergeRows][kMergeFastElems];
+    Acc m = INFINITY;
+    int bad = 0;
+#pragma unroll
+    for (int i = 0; i < kMergeRows; ++i) {
+      const int r = threadIdx.x + i * BLOCK;
+      rr[i] = INFINITY;
+#pragma unroll
+      for (int j = 0; j < kMergeFastElems; ++j) x[i][j] = 0.0;
+      if (r < n) {
+        const Acc* pr = P + static_cast<size_t>(r) * stride;
+        rr[i] = __ldcg(pr);
+        bad |= (__ldcg(pr + 2) != 0.0);
+#pragma unroll
+        for (int j = 0; j < kMergeFastElems; ++j) {
+          const int e = e0 + j * estep;
+          if (e < stride) x[i][j] = __ldcg(pr + e);
+        }
+        m = (rr[i] < m) ? rr[i] : m;
+      }
+    }
+    m = warp_min(m);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = m;
+    bad = __syncthreads_or(bad);
+    Acc rho = s_part[0];
+    for (int w = 1; w < BLOCK / 32; ++w) rho = (s_part[w] < rho) ? s_part[w] : rho;
+    if (e0 == 0 && threadIdx.x == 0) {
+      merged[0] = rho;
+      merged[2] = bad ? 1.0 : 0.0;
+      merged[3] = 0.0;
+    }
+    const double inv_lambda = 1.0 / lambda;
+    Acc acc[kMergeElems];  // (block_sum_n reduces kMergeElems; the rest stay 0)
+#pragma unroll
+    for (int j = 0; j < kMergeElems; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMergeRows; ++i) {
+      if (threadIdx.x + i * BLOCK < n) {
+        const Acc sc = static_cast<double>(__expf(static_cast<float>(-(rr[i] - rho) * inv_lambda)));
+#pragma unroll
+        for (int j = 0; j < kMergeFastElems; ++j) acc[j] = fma(sc, x[i][j], acc[j]);
+      }
+    }
+    block_sum_n<BLOCK>(acc, s_part + BLOCK / 32);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int j = 0; j < kMergeFastElems; ++j) {
+        const int e = e0 + j * estep;
+        if (e < stride && (e == 1 || e >= kPartialHeader)) merged[e] = acc[j];
+      }
+    return;
+  }
   Acc m = INFINITY;
   int bad = 0;
 #pragma unroll 8
