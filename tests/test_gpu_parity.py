@@ -234,18 +234,25 @@ def test_optimize_and_compute_control_slide():
     assert np.array_equal(u, np.clip(before[0], -1, 1))
 
 
-def test_nonfinite_cost_raises_and_leaves_state():
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_nonfinite_cost_raises_and_leaves_state(prec):
     w = c0(samples=256)
-    g = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox")
+    g = Controller(w.params, w.bounds, w.sg, w.cost, precision=prec, noise="philox")
     bad = MlpWeights.zeros(32)
-    bad.b3[:] = 1e308
+    bad.b3[:] = 1e308 if prec == "fp64" else 1e30
     g.set_mlp(bad)
     g.set_costmap(w.costmap)
     U = np.full((100, 2), 0.1)
     g.plan = U
     with pytest.raises(NonFiniteCost):
         g.mpc_step(w.x0[0])
-    assert np.array_equal(g.plan, U) and g.iteration == 0
+    stored = U if prec == "fp64" else U.astype(np.float32).astype(np.float64)  # the fp32 build keeps a float plan
+    assert np.array_equal(g.plan, stored) and g.iteration == 0
+    # the failure does not stick: with sane weights the next step runs (the
+    # step graph carries no status reset; the failed call cleared it)
+    g.set_mlp(w.mlp)
+    u = g.mpc_step(w.x0[0])
+    assert np.all(np.isfinite(u)) and g.iteration == 1
 
 
 # --------------------------------------------------------- closed loop/fleet
@@ -265,24 +272,28 @@ def test_fleet_controllers_are_independent():
     """A fleet handle (BASELINE c3 shape) equals independent single-controller handles."""
     w = workload.make("c3", samples=512, controllers=3)
 
-    def single(c):
-        s = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox")
+    def single(c, prec="fp64"):
+        s = Controller(w.params, w.bounds, w.sg, w.cost, precision=prec, noise="philox")
         s.set_mlp(w.mlp)
         s.set_costmap(w.costmap)
         s.set_seed(w.params.seed + c)  # fleet controller c uses seed + c
         return s
 
-    g = Controller(w.params, w.bounds, w.sg, w.cost, precision="fp64", noise="philox", n_controllers=3)
-    g.set_mlp(w.mlp)
-    g.set_costmap(w.costmap)
-    for _ in range(2):
-        ug = g.mpc_step(w.x0)
-    for c in range(3):
-        s = single(c)
+    # mpc_step: the fp64 generic path and the fp32 tensor-core path (whose
+    # tail writes every controller's host status directly)
+    for prec in ("fp64", "fp32"):
+        g = Controller(w.params, w.bounds, w.sg, w.cost, precision=prec, noise="philox", n_controllers=3)
+        g.set_mlp(w.mlp)
+        g.set_costmap(w.costmap)
         for _ in range(2):
-            us = s.mpc_step(w.x0[c])
-        assert np.array_equal(us, ug[c])
-        assert np.array_equal(s.plan, g.get_plan(c))
+            ug = g.mpc_step(w.x0)
+        for c in range(3):
+            s = single(c, prec)
+            for _ in range(2):
+                us = s.mpc_step(w.x0[c])
+            assert np.array_equal(us, ug[c]), (prec, c)
+            assert np.array_equal(s.plan, g.get_plan(c)), (prec, c)
+            assert s.iteration == g.get_iteration(c) == 2
     # the receding-horizon loop on the device (sticky per-controller status
     # across iterations): every fleet member equals its own single-controller
     # loop, on the fp64 generic path and on the fp32 tensor-core path
