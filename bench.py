@@ -3,12 +3,19 @@
 
 Workload (BASELINE.json configs[1], "c1"): K = 16384 samples, T = 100, 6-32-32-4
 tanh MLP vehicle, 2000 x 2000 elliptical-track costmap, receding horizon with
-the device plant; all inputs synthetic from a seed (see
-paper_1707_02342_b200/workload.py).  Samples shard over the ranks of a
-torchrun launch (one NCCL all-gather of per-chunk softmin partials per
-iteration); ``value`` is whole-job sample-timesteps/s.
+the device plant; all inputs synthetic from a seed (workload.py).  With
+``--gpus N`` the samples of the controller are sharded over N ranks, one
+process per GPU (bench.py launches them itself through torch.distributed.run
+unless it already runs under torchrun): one NCCL all-gather of the fixed group
+rows per iteration (group.cuh).  ``value`` is whole-job sample-timesteps/s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+``--impl reference`` times the reference's own algorithm on the host cores:
+oracle/build/mppi_ref_bench, the double-precision restatement of
+controller.cpp:55-148 with the reference sampler and its std::thread chunks
+(the reference itself cannot be built here: Eigen3 is absent).  That arm
+imports nothing from the product package and loads no CUDA library.
 
 Prints ONE JSON line on rank 0.
 """
@@ -22,16 +29,32 @@ import statistics
 import subprocess
 import sys
 import threading
-import time
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
 
 METRIC = "MPPI iteration latency (ms) and rollout sample-timesteps/sec at 1/2/4/8 B200"
 UNIT = "sample-timesteps/s"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+REF_BENCH = os.path.join(ROOT, "oracle", "build", "mppi_ref_bench")
+SEED = 1707_02342
+
+# BASELINE.json configs as plain data (the same table as
+# paper_1707_02342_b200/workload.py CONFIGS, checked by
+# tests/test_bench_contract.py): the reference arm reads this copy so that it
+# imports nothing from the product package.
+BENCH_CONFIGS = {
+    "c0": dict(samples=1920, horizon_steps=100, hidden=32, controllers=1),
+    "c1": dict(samples=16384, horizon_steps=100, hidden=32, controllers=1),
+    "c2": dict(samples=65536, horizon_steps=150, hidden=64, controllers=1),
+    "c3": dict(samples=2048, horizon_steps=100, hidden=32, controllers=512),
+    "c4": dict(samples=1024, horizon_steps=100, hidden=32, controllers=1),
+}
+SAMPLING = dict(dt=0.02, sigma0=0.3 ** 2, sigma1=0.35 ** 2, lambda_=6.66, gamma=0.1 * 6.66, explore=0.01,
+                sg_window=9, sg_degree=2)
+# CostParams.baseline(): 200 h + (v_x - 6)^2 + 10000 [h > 1 or |roll| > 0.6]
+BASELINE_COST = (200.0, 1.0, 0.0, 6.0, 0.0, 1.0, 1.0, 0.75, 10000.0, 1.0, 0.6)
 
 
 def parse():
@@ -39,7 +62,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c1")
+    ap.add_argument("--config", default="c1", choices=sorted(BENCH_CONFIGS))
     ap.add_argument("--samples", type=int, default=None, help="override K (c4 sweep)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,6 +74,84 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def workload_shape(args):
+    c = dict(BENCH_CONFIGS[args.config])
+    if args.samples is not None:
+        c["samples"] = args.samples
+    return c
+
+
+def config_dict(args, world):
+    """The `config` object of both arms (same keys and values)."""
+    c = workload_shape(args)
+    K, T, H, C = c["samples"], c["horizon_steps"], c["hidden"], c["controllers"]
+    fleet = C > 1
+    return {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, H={H}, MLP vehicle, receding horizon"
+                        + (f", fleet of {C} controllers (perturbed maps)" if fleet else ""),
+            "samples": K, "horizon": T, "hidden": H, "controllers": C,
+            "parallelism": (f"{C // world} independent controllers per GPU on {world} GPU(s), no communication"
+                            if fleet else f"samples sharded over {world} GPU(s)"),
+            "l2": "flushed between timed iterations (256 MiB memset, excluded from timing)"}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------- CPU arm ---
+def ref_bench(shape, threads, steps, warmup):
+    """Run oracle/build/mppi_ref_bench (reference algorithm, fp64, host cores)."""
+    if not os.path.exists(REF_BENCH):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True, capture_output=True)
+    s = SAMPLING
+    cmd = [REF_BENCH, "--samples", str(shape["samples"]), "--horizon", str(shape["horizon_steps"]),
+           "--hidden", str(shape["hidden"]), "--threads", ",".join(str(t) for t in threads), "--steps", str(steps),
+           "--warmup", str(warmup), "--dt", repr(s["dt"]), "--lambda", repr(s["lambda_"]), "--gamma",
+           repr(s["gamma"]), "--sigma0", repr(s["sigma0"]), "--sigma1", repr(s["sigma1"]), "--explore",
+           repr(s["explore"]), "--seed", str(SEED), "--sg-window", str(s["sg_window"]), "--sg-degree",
+           str(s["sg_degree"]), "--cost", ",".join(repr(v) for v in BASELINE_COST)]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return json.loads(out.stdout)
+
+
+def cpu_sample_text(shape, run):
+    fleet = shape["controllers"] > 1
+    return (f"{run['steps']} timed mpc_step calls after {run['warmup']} warm-up calls (steady_clock, median; "
+            f"acceptance.cpp:381-389) on the FULL K={shape['samples']}, T={shape['horizon_steps']}, "
+            f"H={shape['hidden']}"
+            + (" (one controller of the fleet: the CPU runs controllers one after another)" if fleet else "")
+            + f", fp64, reference splitmix64 noise, {run['threads']} std::threads per call; reference algorithm "
+              "restated in oracle/mppi_oracle.cpp (the reference needs Eigen3, absent)")
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    shape = workload_shape(args)
+    threads = cpu_threads()
+    res = ref_bench(shape, [threads], args.steps, args.warmup)
+    run = res["runs"][0]
+    K, T = shape["samples"], shape["horizon_steps"]
+    value = K * T / (run["median_ms"] * 1e-3)
+    ms = sorted(run["ms"])
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": run["median_ms"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Xavier MLP, 2000x2000 ellipse map, "
+                                                          "reference splitmix64 noise)",
+            "impl": "reference", "config": config_dict(args, world),
+            "latency_ms": {"p50": float(np.percentile(ms, 50)), "p99": float(np.percentile(ms, 99)),
+                           "mean": float(np.mean(ms))},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": run["threads"], "kind": "port",
+                             "sample": cpu_sample_text(shape, run)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm -----
 class ClockSampler:
     """SM clocks + throttle reasons sampled through NVML every few ms during the
     timed region (nvidia-smi itself is too slow for a sub-second region; it
@@ -115,82 +216,45 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
-def reference_cpu(w, steps, warmup, sample_k):
-    """The reference CPU path (oracle restatement: double, splitmix noise, std::thread
-    chunks per call, serial sampling/weights/update) on a bounded sample of the workload."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle  # test infrastructure; the CPU arm only
-    from paper_1707_02342_b200.api import SamplingParams
-    p = SamplingParams(**{**w.params.__dict__, "samples": sample_k})
-    o = oracle.OracleController(p, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp64", noise="ref_splitmix",
-                                system=w.system)
-    if w.theta is not None:
-        o.set_basis(w.theta)
-    else:
-        o.set_mlp(w.mlp)
-    o.set_costmap(w.costmap)
-    threads = cpu_threads()
-    x = w.x0[0].copy()
-    times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        u = o.mpc_step(x, threads=threads)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-        x = o.vehicle_step(x, u)
-    med = statistics.median(times)
-    return {"value": sample_k * w.params.horizon_steps / med, "unit": UNIT, "cores": threads, "kind": "port",
-            "ms_per_step": med * 1e3, "total_s": sum(times),
-            "sample": f"{len(times)} mpc_step calls on {sample_k} of the {w.params.samples} samples, "
-                      f"T={w.params.horizon_steps}, fp64, reference splitmix noise, {threads} std::threads"}
-
-
-def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
-        return
-    from paper_1707_02342_b200 import workload
-    w = workload.make(args.config, samples=args.samples)
-    sample_k = min(w.params.samples, 2048)
-    steps = max(1, min(args.steps, 60))
-    warm = max(1, min(args.warmup, 3))
-    cb = reference_cpu(w, steps, warm, sample_k)
-    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-            "warmup": warm, "ms_per_step": cb["ms_per_step"] * (w.params.samples / sample_k),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"{args.config}: K={w.params.samples}, T={w.params.horizon_steps}, H={w.hidden}",
-                       "parallelism": f"{cb['cores']} CPU threads"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def load_traffic():
+def load_ncu_summary():
+    """Per-launch DRAM bytes and XU (SFU) warp-instructions of K1 from the
+    committed ncu --set full capture (profiles/ncu_rollout_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_rollout_summary.json")
     try:
-        d = json.load(open(p))
-        return d.get("dram_bytes_per_launch"), d.get("source")
+        return json.load(open(p))
     except Exception:
-        return None, None
+        return {}
+
+
+def spawn_ranks(args):
+    """--gpus N outside torchrun: launch N ranks of this script (one process per GPU)."""
+    import socket
+    import torch
+    n_dev = torch.cuda.device_count()
+    if n_dev < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} needs {args.gpus} GPUs, {n_dev} visible"}),
+              flush=True)
+        sys.exit(2)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def run_ours(args):
-    import torch
-    from paper_1707_02342_b200 import workload
-    from paper_1707_02342_b200.api import Controller, fp32_peak_tflops
-
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args)
     if world != args.gpus:
-        args.gpus = world
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without torchrun to let bench.py spawn the ranks)")
+    import torch
+    sys.path.insert(0, ROOT)
+    from paper_1707_02342_b200 import workload
+    from paper_1707_02342_b200.api import Controller, fp32_peak_tflops, pipe_peaks
+
     torch.cuda.set_device(local)
     pg = None
     if world > 1:
@@ -198,20 +262,23 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
 
+    shape = workload_shape(args)
     w = workload.make(args.config, samples=args.samples)
+    assert (w.params.samples, w.params.horizon_steps, w.hidden, w.controllers) == (
+        shape["samples"], shape["horizon_steps"], shape["hidden"], shape["controllers"])
     fleet = w.controllers > 1
     # fleet (c3): the independent controllers are split over the ranks, no
-    # communicator; otherwise the samples of one controller are sharded
-    C = max(1, w.controllers // world) if fleet else 1
+    # communicator, seeds and map perturbations keyed by the global controller
+    # index; otherwise the samples of one controller are sharded
+    if fleet and w.controllers % world:
+        raise SystemExit(f"bench.py: {w.controllers} controllers do not split over {world} GPUs")
+    C = w.controllers // world if fleet else 1
     ctrl = Controller(w.params, w.bounds, w.sg, w.cost, hidden=w.hidden, precision="fp32", noise="philox",
-                      device=local, n_controllers=C, system=w.system)
-    if w.theta is not None:
-        ctrl.set_basis(w.theta)
-    else:
-        ctrl.set_mlp(w.mlp)
+                      device=local, n_controllers=C, system=w.system, controller_offset=rank * C if fleet else 0)
+    ctrl.set_mlp(w.mlp)
     ctrl.set_costmap(w.costmap)
     if fleet:
-        ctrl.perturb_fleet_costmaps(0.02, workload.SEED + rank)  # per-controller N(0, 0.02^2) map noise
+        ctrl.perturb_fleet_costmaps(0.02, workload.SEED)  # per-controller N(0, 0.02^2) map noise
     elif world > 1:
         obj = [Controller.nccl_unique_id() if rank == 0 else None]
         pg.broadcast_object_list(obj, src=0)
@@ -226,27 +293,32 @@ def run_ours(args):
             pg.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(values):
+        t = torch.tensor(values, dtype=torch.float64, device="cuda")
+        if pg:
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return t.cpu().numpy()
+
     # warm-up (graphs captured, clocks up)
     ctrl.closed_loop_timed(x0, max(3, args.warmup), L2_FLUSH_BYTES)
-    ctrl.profile_read(reset=True)
     barrier()
     n_launch0 = ctrl.launch_count
     with ClockSampler(local) as clocks:
-        ms = ctrl.closed_loop_timed(x0, args.steps, L2_FLUSH_BYTES)
+        ms, iter_ms = ctrl.closed_loop_timed(x0, args.steps, L2_FLUSH_BYTES, per_iteration=True)
     barrier()
     launches = ctrl.launch_count - n_launch0
-    # K1's own launch duration (roofline): a separate pass of the iteration
-    # graph that brackets K1 with event nodes (not in the timed region: those
-    # nodes would cut the tail's programmatic-launch edge to K1)
+    # K1's own launch duration (roofline) and the exchange time: a separate pass
+    # of the iteration graph with event nodes around K1 and the all-gather (not
+    # in the timed region: those nodes cut the programmatic-launch edges)
     ctrl.profile(True)
     ctrl.profile_read(reset=True)
+    ctrl.profile_read_exchange(reset=True)
     ctrl.closed_loop_timed(x0, min(args.steps, 50), L2_FLUSH_BYTES)
     k1_ms, k1_n = ctrl.profile_read(reset=True)
+    x_ms, x_n = ctrl.profile_read_exchange(reset=True)
     ctrl.profile(False)
-    t = torch.tensor([ms, k1_ms / max(k1_n, 1)], dtype=torch.float64, device="cuda")
-    if pg:
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-    ms_max, k1_avg_ms = float(t[0]), float(t[1])
+    red = max_over_ranks([ms, k1_ms / max(k1_n, 1), x_ms / max(x_n, 1)] + list(iter_ms))
+    ms_max, k1_avg_ms, x_avg_ms, iters_max = float(red[0]), float(red[1]), float(red[2]), red[3:]
     ms_per_step = ms_max / args.steps
     units_per_step = (C * world if fleet else 1) * K * T  # sample-steps of the whole job per iteration
     value = units_per_step * args.steps / (ms_max * 1e-3)
@@ -279,54 +351,73 @@ def run_ours(args):
                 x[:, 4] = vx + 0.5 * u[:, 1] * dt
         ev1.record(stream)
         ev1.synchronize()
-        e_ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
-        if pg:
-            pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
-        e_ms = float(e_ms[0])
+        e_ms = float(max_over_ranks([ev0.elapsed_time(ev1)])[0])
         e2e = {"value": units_per_step * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
                "h2d_bytes_per_step": C * 8 * 4, "d2h_bytes_per_step": C * 96,
-               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H (written to pinned host memory by the tail kernel)"}
+               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H "
+                       "(written to pinned host memory by the tail kernel)"}
 
     if rank != 0:
         if pg:
             pg.destroy_process_group()
         return
 
-    # algorithmic FLOPs per sample-step: the MLP GEMVs, or Theta^T phi (25 x 4) of the basis model
-    flop_unit = 2 * 25 * 4 if w.theta is not None else workload.flops_per_sample_step(w.hidden)
-    k_local = K * C if fleet else (K // world if world > 1 else K)
+    # ---- roofline of K1: FP32 (the north star's), tensor (mma f16x3) and SFU ceilings
+    flop_unit = workload.flops_per_sample_step(w.hidden)
+    info = ctrl.shard_info
+    chunk = max(1, -(-K // info["chunks"]))
+    k_local = K * C if fleet else min(K, (info["chunk_hi"] - info["chunk_lo"]) * chunk)
     k1_flops = k_local * T * flop_unit
-    peak, clk = fp32_peak_tflops(local)
+    peak, _ = fp32_peak_tflops(local)
+    hmma_tflops, mufu_gops = pipe_peaks(local)
     achieved = k1_flops / (k1_avg_ms * 1e-3) / 1e12 if k1_avg_ms > 0 else None
-    traffic, traffic_src = load_traffic()
+    ncu = load_ncu_summary()
+    same_shape = ncu.get("samples") == K and ncu.get("horizon") == T and ncu.get("hidden") == w.hidden and not fleet \
+        and world == 1
+    xu_per_ss = ncu.get("xu_warp_inst_per_launch", 0) * 32 / (ncu["samples"] * ncu["horizon"]) \
+        if ncu.get("xu_warp_inst_per_launch") else None
+    sfu_frac = (xu_per_ss * k_local * T / (k1_avg_ms * 1e-3) / (mufu_gops * 1e9)) \
+        if (xu_per_ss and k1_avg_ms > 0 and mufu_gops > 0) else None
+    tensor_peak = hmma_tflops / 3.0  # three fp16 products (hi*hi + hi*lo + lo*hi) per fp32 MAC
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and not fleet:
-        cb = reference_cpu(w, steps=3, warmup=1, sample_k=min(K, 2048))
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if not args.no_cpu_baseline and world == 1:
+        shape1 = dict(shape)
+        res = ref_bench(shape1, [1, cpu_threads()], 7, 2)
+        runs = {r["threads"]: r for r in res["runs"]}
+        allc = runs[cpu_threads()]
+        one = runs[1]
+        cpu = {"value": allc["sample_steps_per_s"], "unit": UNIT, "cores": allc["threads"], "kind": "port",
+               "sample": cpu_sample_text(shape1, allc), "ms_per_step": allc["median_ms"],
+               "single_thread": {"value": one["sample_steps_per_s"], "cores": 1, "ms_per_step": one["median_ms"]}}
+    it = np.asarray(iters_max)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         # the total work (K samples of one controller, or the 512-controller
         # fleet) is fixed and split over the GPUs
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Xavier MLP, 2000x2000 ellipse map, Philox noise)",
-        "config": {"workload": f"{args.config}: IT-MPPI iteration, K={K}, T={T}, "
-                               + ("basis-function vehicle (reference acceptance #10 shape), "
-                                  if w.theta is not None else f"H={w.hidden}, MLP vehicle, ") +
-                               f"receding horizon with device plant"
-                               + (f", fleet of {C * world} controllers (perturbed maps)" if fleet else ""),
-                   "samples": K, "horizon": T, "hidden": w.hidden, "controllers": C * world,
-                   "parallelism": (f"{C} independent controllers per GPU on {world} GPU(s), no communication"
-                                   if fleet else f"samples sharded over {world} GPU(s)"),
-                   "l2": "flushed between timed iterations (256 MiB memset, excluded from timing)",
-                   "kernel": ctrl.kernel_variant},
+        "config": dict(config_dict(args, world), kernel=ctrl.kernel_variant),
+        "latency_ms": {"p50": float(np.percentile(it, 50)), "p99": float(np.percentile(it, 99)),
+                       "mean": float(it.mean()), "max": float(it.max()),
+                       "note": "per-iteration CUDA-event intervals of the timed loop, max over ranks"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                     "kernel": "rollout_kernel (K1)", "k1_ms_per_launch": k1_avg_ms,
+                     "frac": (achieved / peak) if (achieved and peak) else None,
+                     "traffic": ncu.get("dram_bytes_per_launch") if same_shape else None,
+                     "kernel": "rollout_tc_kernel (K1)", "k1_ms_per_launch": k1_avg_ms,
                      "k1_share_of_step": k1_avg_ms / ms_per_step if ms_per_step else None,
                      "flop_per_launch": k1_flops, "flop_per_sample_step": flop_unit,
                      "peak_source": "measured FFMA/FFMA2 probe on this GPU (mppi_gpu_fp32_peak_probe); "
                                     "MEASURED_PEAKS.json has no FP32 CUDA-core figure",
-                     "traffic_source": traffic_src},
+                     "ceilings": {
+                         "tensor_mma_f16x3": {"peak_tflops": tensor_peak, "frac": achieved / tensor_peak
+                                              if (achieved and tensor_peak) else None,
+                                              "note": "measured mma.sync m16n8k16 f16 peak / 3 (the fp16x3 split)"},
+                         "sfu": {"peak_gops": mufu_gops, "xu_lane_ops_per_sample_step": xu_per_ss, "frac": sfu_frac,
+                                 "note": "XU instructions per sample-step from the ncu capture x K1 units / K1 time "
+                                         "vs the measured MUFU ex2 peak"},
+                     },
+                     "traffic_source": ncu.get("source") if same_shape else None},
+        "exchange_ms_per_iteration": x_avg_ms if world > 1 else 0.0,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
         "iteration_latency_ms": ms_per_step,
     }

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define MPPI_GPU_ABI_VERSION 1
+#define MPPI_GPU_ABI_VERSION 2
 
 /* Status codes.  The C++ wrapper maps them to the reference's exceptions:
  * INVALID_ARGUMENT and NONFINITE -> std::invalid_argument (types.hpp:105-122,
@@ -80,7 +80,8 @@ enum { MPPI_FP32 = 0, MPPI_FP64 = 1 };
  * dynamics.cpp:152-157), with the same costs as VEHICLE_MLP. */
 enum { MPPI_SYSTEM_VEHICLE_MLP = 0, MPPI_SYSTEM_QUADRATIC = 1, MPPI_SYSTEM_VEHICLE_BASIS = 2 };
 
-/* Weight rule (controller.hpp:32). Only IT is implemented on the device. */
+/* Weight rule (controller.hpp:32): information-theoretic softmin or CEM
+ * elite averaging (weights.cpp:8-53), both on the device. */
 enum { MPPI_WEIGHT_IT = 0, MPPI_WEIGHT_CEM = 1 };
 
 /* Driving cost, CostParams (costs.hpp:46-64) plus the BASELINE crash form:
@@ -132,6 +133,11 @@ typedef struct mppi_gpu_config {
   int32_t device;           /* CUDA device ordinal */
   double quad_cost_scale;   /* QUADRATIC only */
   mppi_cost_params cost;
+  /* Global index of controller 0 of this handle (a fleet split over ranks):
+   * controller i draws noise from seed + controller_offset + i and its fleet
+   * map perturbation from stream controller_offset + i, so the fleet is the
+   * same workload at every rank count. */
+  int32_t controller_offset;
 } mppi_gpu_config;
 
 typedef struct mppi_gpu_handle mppi_gpu_handle;
@@ -210,9 +216,10 @@ int mppi_gpu_closed_loop(mppi_gpu_handle* h, const double* x_init, int iteration
  * handle's stream.  flush_l2_bytes > 0 overwrites a scratch buffer of that
  * size between iterations (evicting L2) and then sums the per-iteration event
  * intervals, so the flush is excluded from device_ms_out; 0 times the whole
- * back-to-back loop. */
+ * back-to-back loop.  iter_ms_out (nullable, flush mode only) receives the
+ * `iterations` per-iteration intervals (p50 / p99 latency). */
 int mppi_gpu_closed_loop_timed(mppi_gpu_handle* h, const double* x_init, int iterations,
-                               uint64_t flush_l2_bytes, double* device_ms_out);
+                               uint64_t flush_l2_bytes, double* device_ms_out, double* iter_ms_out);
 
 /* ---- parity entry points (controller 0) ------------------------------------ */
 /* sample_perturbations(params, iteration) (sampler.cpp:5-39) evaluated on the
@@ -239,13 +246,38 @@ int mppi_gpu_rollout_states(mppi_gpu_handle* h, const double* x0, int sample,
                             double* states_out);
 
 /* ---- multi-GPU: shard samples over ranks, one exchange per iteration ------- */
+/* The samples of one controller are cut into chunks, and the chunks into G
+ * fixed groups (G = 8 * 2^j, set by the chunk count alone).  Every group's
+ * chunk partials (rho, eta, T x 2 weighted-noise numerator) are merged on the
+ * device into one group row, in a fixed order; rank r of N owns groups
+ * [r G/N, (r+1) G/N).  The exchange is one all-gather of the group rows
+ * (G x (4 + 2T) doubles for the whole job), after which every rank merges
+ * them in group order: the plan is bit-identical on every rank and for every
+ * N dividing G, including N = 1 (parallel_for_chunks, parallel.hpp:11-29). */
 /* 128-byte ncclUniqueId, created on rank 0 and broadcast by the caller. */
 int mppi_gpu_nccl_unique_id(unsigned char id_out[128]);
-/* Rank r of world_size owns a contiguous range of sample chunks; per-chunk
- * softmin partials are all-gathered and merged in global chunk order, so the
- * plan is bit-identical on every rank and to the single-GPU result. */
+/* NCCL sharding: this handle becomes rank `rank` of `world_size` (one handle
+ * per process and GPU).  MPPI_ERR_UNSUPPORTED if world_size does not divide
+ * G, for fleets (n_controllers > 1) and for the CEM rule.  A rejected call
+ * leaves the handle unchanged. */
 int mppi_gpu_set_comm(mppi_gpu_handle* h, int rank, int world_size,
                       const unsigned char id[128]);
+/* In-process sharding: handles[r] becomes rank r of n (one handle per GPU of
+ * this process, or several handles on one GPU).  The exchange copies the
+ * other ranks' group rows device to device.  Every handle needs the same
+ * configuration; destroying one leaves the others unusable for step_local. */
+int mppi_gpu_set_comm_local(mppi_gpu_handle** handles, int n);
+/* mpc_step of a controller sharded with set_comm_local: every rank's rollout
+ * and group merge, then every rank's exchange and epilogue.  x0 is the one
+ * state (state_dim doubles) all ranks use; u0_out receives n x 2 (every
+ * rank's u0; they are identical). */
+int mppi_gpu_step_local(mppi_gpu_handle** handles, int n, const double* x0, double* u0_out);
+/* The handle's partition: {rank, world_size, chunks, groups, chunk_lo,
+ * chunk_hi, group_lo, group_hi} (chunk and group ranges of this rank). */
+int mppi_gpu_shard_info(mppi_gpu_handle* h, int32_t out[8]);
+/* The same partition as a pure function (no device): chunk_samples is the K1
+ * chunk size of the handle's kernel variant. */
+int mppi_gpu_shard_plan(int samples, int chunk_samples, int rank, int world_size, int32_t out[8]);
 
 /* ---- instrumentation ------------------------------------------------------- */
 /* cudaStream_t of the handle (for CUDA-event timing on the launching stream). */
@@ -257,11 +289,19 @@ int mppi_gpu_launch_count(mppi_gpu_handle* h, uint64_t* count_out);
 int mppi_gpu_profile_enable(mppi_gpu_handle* h, int enable);
 int mppi_gpu_profile_read(mppi_gpu_handle* h, double* rollout_ms, uint64_t* rollout_launches,
                           int reset);
+/* With profiling enabled and world_size > 1: CUDA-event time of the group-row
+ * exchange (the all-gather) summed over the timed closed-loop iterations. */
+int mppi_gpu_profile_read_exchange(mppi_gpu_handle* h, double* exchange_ms, uint64_t* exchanges,
+                                   int reset);
 /* Name of the rollout kernel variant the handle dispatches. */
 int mppi_gpu_kernel_variant(mppi_gpu_handle* h, char* name_out, int capacity);
 /* FFMA microbenchmark on `device`: best measured FP32 FMA throughput
  * (TFLOP/s, FMA = 2 FLOP) over the probe variants; the roofline denominator. */
 int mppi_gpu_fp32_peak_probe(int device, double* tflops_out, double* sm_clock_mhz_out);
+/* Tensor and SFU ceilings of the tensor-core rollout on `device`: mma.sync
+ * m16n8k16 f16 -> f32 throughput (TFLOP/s) and MUFU ex2 throughput (G lane
+ * operations/s), the best of a few full-chip probe launches. */
+int mppi_gpu_pipe_peak_probe(int device, double* hmma_tflops_out, double* mufu_gops_out);
 
 /* ---- host-side workload generation (no GPU needed) ------------------------- */
 /* Xavier-uniform MLP weights from a seed (BASELINE configs): U(-a, a),

@@ -98,6 +98,7 @@ class ConfigC(ctypes.Structure):
         ("device", c_int32),
         ("quad_cost_scale", c_double),
         ("cost", CostParamsC),
+        ("controller_offset", c_int32),
     ]
 
 
@@ -127,7 +128,7 @@ _SIGNATURES = {
     "mppi_gpu_step": (c_int, [c_void_p, _d, _d]),
     "mppi_gpu_optimize": (c_int, [c_void_p, _d, c_int]),
     "mppi_gpu_closed_loop": (c_int, [c_void_p, _d, c_int, _d, _d]),
-    "mppi_gpu_closed_loop_timed": (c_int, [c_void_p, _d, c_int, c_uint64, _d]),
+    "mppi_gpu_closed_loop_timed": (c_int, [c_void_p, _d, c_int, c_uint64, _d, _d]),
     "mppi_gpu_sample_perturbations": (c_int, [c_void_p, c_uint64, _d, _P(c_uint8)]),
     "mppi_gpu_rollout_costs": (c_int, [c_void_p, _d, _d, _d, _d]),
     "mppi_gpu_weights": (c_int, [c_void_p, _d, _d, _d, _d]),
@@ -135,12 +136,18 @@ _SIGNATURES = {
     "mppi_gpu_rollout_states": (c_int, [c_void_p, _d, c_int, _d]),
     "mppi_gpu_nccl_unique_id": (c_int, [_P(c_uint8)]),
     "mppi_gpu_set_comm": (c_int, [c_void_p, c_int, c_int, _P(c_uint8)]),
+    "mppi_gpu_set_comm_local": (c_int, [_P(c_void_p), c_int]),
+    "mppi_gpu_step_local": (c_int, [_P(c_void_p), c_int, _d, _d]),
+    "mppi_gpu_shard_info": (c_int, [c_void_p, _P(c_int32)]),
+    "mppi_gpu_shard_plan": (c_int, [c_int, c_int, c_int, c_int, _P(c_int32)]),
+    "mppi_gpu_profile_read_exchange": (c_int, [c_void_p, _d, _P(c_uint64), c_int]),
     "mppi_gpu_get_stream": (c_int, [c_void_p, _P(c_void_p)]),
     "mppi_gpu_launch_count": (c_int, [c_void_p, _P(c_uint64)]),
     "mppi_gpu_profile_enable": (c_int, [c_void_p, c_int]),
     "mppi_gpu_profile_read": (c_int, [c_void_p, _d, _P(c_uint64), c_int]),
     "mppi_gpu_kernel_variant": (c_int, [c_void_p, ctypes.c_char_p, c_int]),
     "mppi_gpu_fp32_peak_probe": (c_int, [c_int, _d, _d]),
+    "mppi_gpu_pipe_peak_probe": (c_int, [c_int, _d, _d]),
     "mppi_workload_mlp_xavier": (c_int, [c_int, c_uint64, c_double, _d, _d, _d, _d, _d, _d]),
     "mppi_workload_ellipse_costmap": (c_int, [c_int, c_int, c_double, c_double, c_double, c_double,
                                               c_double, c_double, _P(c_float)]),

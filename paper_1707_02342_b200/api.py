@@ -240,6 +240,13 @@ def device_count() -> int:
     return int(_lib.load().mppi_gpu_device_count())
 
 
+def pipe_peaks(device: int = 0):
+    """Measured mma.sync f16 peak (TFLOP/s) and MUFU ex2 peak (G lane-ops/s)."""
+    t, m = ctypes.c_double(), ctypes.c_double()
+    check(_lib.load().mppi_gpu_pipe_peak_probe(device, ctypes.byref(t), ctypes.byref(m)))
+    return t.value, m.value
+
+
 def fp32_peak_tflops(device: int = 0):
     """Measured FP32 FMA peak (TFLOP/s) and the device max SM clock (MHz)."""
     t, mhz = ctypes.c_double(), ctypes.c_double()
@@ -253,12 +260,23 @@ _SYSTEM = {"vehicle_mlp": _lib.SYSTEM_VEHICLE_MLP, "quadratic": _lib.SYSTEM_QUAD
            "vehicle_basis": _lib.SYSTEM_VEHICLE_BASIS}
 
 
+SHARD_KEYS = ("rank", "world_size", "chunks", "groups", "chunk_lo", "chunk_hi", "group_lo", "group_hi")
+
+
+def shard_plan(samples: int, chunk_samples: int, rank: int, world_size: int) -> dict:
+    """The sample partition of mppi_gpu_set_comm as a pure host function (no
+    device): chunks of ``chunk_samples``, fixed groups, this rank's ranges."""
+    v = (ctypes.c_int32 * 8)()
+    check(_lib.load().mppi_gpu_shard_plan(samples, chunk_samples, rank, world_size, v))
+    return dict(zip(SHARD_KEYS, list(v)))
+
+
 def make_config(params: SamplingParams, bounds: ControlBounds = ControlBounds(),
                 sg: Optional[SGFilter] = SGFilter(), cost: CostParams = CostParams(), *,
                 system: str = "vehicle_mlp", hidden: int = 32, precision: str = "fp32",
                 noise: str = "philox", n_controllers: int = 1, device: int = 0,
                 with_terminal: bool = True, quad_cost_scale: float = 1.0, weight_rule: str = "it",
-                cem_delta: float = 0.8) -> _lib.ConfigC:
+                cem_delta: float = 0.8, controller_offset: int = 0) -> _lib.ConfigC:
     """mppi_gpu_config from the reference's parameter objects; ``weight_rule``
     "it" (it_weights) or "cem" (cem_weights with ``cem_delta``, the
     WeightRuleConfig of controller.hpp:32-37)."""
@@ -289,6 +307,7 @@ def make_config(params: SamplingParams, bounds: ControlBounds = ControlBounds(),
     cfg.quad_cost_scale = quad_cost_scale
     cfg.weight_rule = {"it": _lib.WEIGHT_IT, "cem": _lib.WEIGHT_CEM}[weight_rule]
     cfg.cem_delta = cem_delta
+    cfg.controller_offset = controller_offset
     for f in CostParams.__dataclass_fields__:
         setattr(cfg.cost, f, float(getattr(cost, f)))
     return cfg
@@ -436,11 +455,14 @@ class Controller:
         check(self._lib.mppi_gpu_closed_loop(self._h, dptr(self._x(x_init)), iterations, dptr(u), dptr(x)))
         return u, x
 
-    def closed_loop_timed(self, x_init, iterations: int, flush_l2_bytes: int = 0) -> float:
+    def closed_loop_timed(self, x_init, iterations: int, flush_l2_bytes: int = 0, per_iteration: bool = False):
+        """Device-timed receding-horizon loop: total ms, or (total ms, per-iteration
+        ms array) with ``per_iteration`` (flush mode only)."""
         ms = ctypes.c_double()
+        it = np.zeros(iterations) if per_iteration else None
         check(self._lib.mppi_gpu_closed_loop_timed(self._h, dptr(self._x(x_init)), iterations, flush_l2_bytes,
-                                                   ctypes.byref(ms)))
-        return ms.value
+                                                   ctypes.byref(ms), dptr(it)))
+        return (ms.value, it) if per_iteration else ms.value
 
     # -- parity entry points ------------------------------------------------
     def sample_perturbations(self, iteration: int):
@@ -492,10 +514,43 @@ class Controller:
         return bytes(buf)
 
     def set_comm(self, rank: int, world_size: int, unique_id: Optional[bytes]) -> None:
+        """NCCL sample sharding: this handle is rank ``rank`` of ``world_size``
+        (mppi_gpu_set_comm; the group rows are all-gathered every iteration)."""
         buf = None
         if unique_id is not None:
             buf = (ctypes.c_uint8 * 128)(*unique_id)
         check(self._lib.mppi_gpu_set_comm(self._h, rank, world_size, buf))
+
+    @staticmethod
+    def set_comm_local(ctrls: Sequence["Controller"]) -> None:
+        """In-process sample sharding: ``ctrls[r]`` becomes rank r (one handle
+        per GPU of this process, or several on one GPU); the exchange is a
+        device-to-device copy of the group rows (mppi_gpu_set_comm_local)."""
+        hs = (ctypes.c_void_p * len(ctrls))(*[c._h.value for c in ctrls])
+        check(_lib.load().mppi_gpu_set_comm_local(hs, len(ctrls)))
+
+    @staticmethod
+    def step_local(ctrls: Sequence["Controller"], x0) -> np.ndarray:
+        """mpc_step of a controller sharded with set_comm_local; returns every
+        rank's u0 (n x 2, identical rows)."""
+        x = np.ascontiguousarray(np.asarray(x0, dtype=np.float64).reshape(-1))
+        u = np.zeros((len(ctrls), 2))
+        hs = (ctypes.c_void_p * len(ctrls))(*[c._h.value for c in ctrls])
+        check(_lib.load().mppi_gpu_step_local(hs, len(ctrls), dptr(x), dptr(u)))
+        return u
+
+    @property
+    def shard_info(self) -> dict:
+        """{rank, world_size, chunks, groups, chunk_lo, chunk_hi, group_lo, group_hi}."""
+        v = (ctypes.c_int32 * 8)()
+        check(self._lib.mppi_gpu_shard_info(self._h, v))
+        return dict(zip(SHARD_KEYS, list(v)))
+
+    def profile_read_exchange(self, reset: bool = True):
+        """(ms, count) of the group-row exchange over the profiled closed-loop iterations."""
+        ms, n = ctypes.c_double(), ctypes.c_uint64()
+        check(self._lib.mppi_gpu_profile_read_exchange(self._h, ctypes.byref(ms), ctypes.byref(n), int(reset)))
+        return ms.value, int(n.value)
 
     # -- instrumentation ----------------------------------------------------
     @property

@@ -11,6 +11,9 @@
 #include "errors.hpp"
 #include "handle_iface.hpp"
 #include "nccl_api.hpp"
+#include "shard.hpp"
+
+#include <vector>
 
 using namespace mppi_host;
 
@@ -71,6 +74,7 @@ void mppi_gpu_config_init(mppi_gpu_config* c) {
   c->cost.crash_penalty = 0.0;
   c->cost.crash_threshold = 1.0;
   c->cost.roll_limit = INFINITY;
+  c->controller_offset = 0;
 }
 
 int mppi_gpu_device_count(void) {
@@ -183,14 +187,16 @@ int mppi_gpu_closed_loop(mppi_gpu_handle* h, const double* x_init, int iteration
                          double* x_trace) {
   return with_handle(h, [&](auto& x) {
     if (!x_init) throw_invalid("closed_loop: null x_init");
-    x.closed_loop(x_init, iterations, u_trace, x_trace, 0, nullptr);
+    x.closed_loop(x_init, iterations, u_trace, x_trace, 0, nullptr, nullptr);
   });
 }
 int mppi_gpu_closed_loop_timed(mppi_gpu_handle* h, const double* x_init, int iterations,
-                               uint64_t flush_l2_bytes, double* device_ms_out) {
+                               uint64_t flush_l2_bytes, double* device_ms_out, double* iter_ms_out) {
   return with_handle(h, [&](auto& x) {
     if (!x_init) throw_invalid("closed_loop: null x_init");
-    x.closed_loop(x_init, iterations, nullptr, nullptr, static_cast<size_t>(flush_l2_bytes), device_ms_out);
+    if (iter_ms_out && flush_l2_bytes == 0) throw_invalid("closed_loop_timed: per-iteration times need flush mode");
+    x.closed_loop(x_init, iterations, nullptr, nullptr, static_cast<size_t>(flush_l2_bytes), device_ms_out,
+                  iter_ms_out);
   });
 }
 int mppi_gpu_sample_perturbations(mppi_gpu_handle* h, uint64_t iteration, double* eps_out,
@@ -236,9 +242,69 @@ int mppi_gpu_nccl_unique_id(unsigned char id_out[128]) {
 }
 int mppi_gpu_set_comm(mppi_gpu_handle* h, int rank, int world_size, const unsigned char id[128]) {
   return with_handle(h, [&](auto& x) {
-    if (world_size > 1 && !id) throw_invalid("set_comm: null id");
     x.set_comm(rank, world_size, id);
   });
+}
+int mppi_gpu_set_comm_local(mppi_gpu_handle** handles, int n) {
+  return guard([&] {
+    if (!handles || n < 1) throw_invalid("set_comm_local: need at least one handle");
+    std::vector<HandleBase*> peers;
+    for (int i = 0; i < n; ++i) {
+      if (!handles[i] || !handles[i]->impl) throw_invalid("set_comm_local: null handle");
+      for (int j = 0; j < i; ++j)
+        if (handles[j] == handles[i]) throw_invalid("set_comm_local: a handle appears twice");
+      peers.push_back(handles[i]->impl.get());
+    }
+    // (rank 0 checks the whole group, so a mismatch is rejected before any commit)
+    for (int r = 0; r < n; ++r) {
+      CUDA_TRY(cudaSetDevice(peers[r]->device_index()));
+      peers[r]->set_comm_local_base(peers, r);
+    }
+  });
+}
+int mppi_gpu_step_local(mppi_gpu_handle** handles, int n, const double* x0, double* u0_out) {
+  return guard([&] {
+    if (!handles || n < 1 || !x0) throw_invalid("step_local: null argument");
+    for (int i = 0; i < n; ++i)
+      if (!handles[i] || !handles[i]->impl) throw_invalid("step_local: null handle");
+    auto on = [&](int r) -> HandleBase& {
+      HandleBase& x = *handles[r]->impl;
+      CUDA_TRY(cudaSetDevice(x.device_index()));
+      return x;
+    };
+    // fronts, a host sync of every rank, then backs: no kernel of one rank
+    // ever waits for another rank's
+    for (int r = 0; r < n; ++r) on(r).local_front(x0);
+    for (int r = 0; r < n; ++r) on(r).sync_stream();
+    for (int r = 0; r < n; ++r) on(r).local_back(true);
+    for (int r = 0; r < n; ++r) on(r).local_finish(u0_out ? u0_out + 2 * r : nullptr);
+  });
+}
+int mppi_gpu_shard_info(mppi_gpu_handle* h, int32_t out[8]) {
+  return with_handle(h, [&](auto& x) {
+    if (!out) throw_invalid("shard_info: null");
+    int v[8];
+    x.shard_info(v);
+    for (int i = 0; i < 8; ++i) out[i] = v[i];
+  });
+}
+int mppi_gpu_shard_plan(int samples, int chunk_samples, int rank, int world_size, int32_t out[8]) {
+  return guard([&] {
+    if (!out) throw_invalid("shard_plan: null");
+    if (samples < 1 || chunk_samples < 1) throw_invalid("shard_plan: samples and chunk_samples must be >= 1");
+    if (world_size < 1 || rank < 0 || rank >= world_size) throw_invalid("shard_plan: bad rank/world_size");
+    const int n_chunks = (samples + chunk_samples - 1) / chunk_samples;
+    const int n_groups = mppi_dev::group_count(n_chunks);
+    if (n_groups % world_size != 0)
+      throw Error(MPPI_ERR_UNSUPPORTED, "shard_plan: world_size must divide the exchange group count");
+    const int g_lo = rank * (n_groups / world_size), g_hi = (rank + 1) * (n_groups / world_size);
+    const int v[8] = {rank, world_size, n_chunks, n_groups, mppi_dev::group_first_chunk(g_lo, n_chunks, n_groups),
+                      mppi_dev::group_first_chunk(g_hi, n_chunks, n_groups), g_lo, g_hi};
+    for (int i = 0; i < 8; ++i) out[i] = v[i];
+  });
+}
+int mppi_gpu_profile_read_exchange(mppi_gpu_handle* h, double* exchange_ms, uint64_t* exchanges, int reset) {
+  return with_handle(h, [&](auto& x) { x.read_exchange_profile(exchange_ms, exchanges, reset != 0); });
 }
 int mppi_gpu_get_stream(mppi_gpu_handle* h, void** stream_out) {
   return with_handle(h, [&](auto& x) {

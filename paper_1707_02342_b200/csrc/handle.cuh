@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "epilogue.cuh"
+#include "group.cuh"
 #include "rollout_tc.cuh"
 #include "cem.cuh"
 #include "ws_launch.hpp"
@@ -89,7 +90,16 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
   };
   // the layer inputs are s = -1/(1 + 2^(kz)) = (tanh z - 1) / 2
   auto B2 = [&](int i, int n) -> double { return 2.0 * kk2 * W2(n, i); };
-  auto B3 = [&](int i, int n) -> double { return n < 4 ? 2.0 * W3(n, i) : 0.0; };
+  // layer 3 on 2^s-scaled weights, max |2 W3| 2^s in [0.5, 1) (TcLayout: keeps
+  // the lo halves of the fp16 split out of the subnormal range)
+  double w3max = 0.0;
+  for (int n = 0; n < 4; ++n)
+    for (int i = 0; i < H; ++i) w3max = std::max(w3max, std::abs(2.0 * W3(n, i)));
+  int s3 = 0;
+  while (s3 < 12 && w3max > 0.0 && w3max * std::ldexp(1.0, s3 + 1) < 1.0) ++s3;
+  if (const char* e = std::getenv("MPPI_TC_W3_SHIFT")) s3 = std::max(0, std::min(12, std::atoi(e)));  // A/B only
+  const double sc3 = std::ldexp(1.0, s3);
+  auto B3 = [&](int i, int n) -> double { return n < 4 ? sc3 * 2.0 * W3(n, i) : 0.0; };
   auto hl = [](double x, int which) -> uint16_t {
     const __half h = __double2half(x);
     if (which == 0) return __half_as_ushort(h);
@@ -135,11 +145,17 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
       if (n < 4) {
         double sum = 0.0;
         for (int i = 0; i < H; ++i) sum += W3(n, i);
-        v = static_cast<float>(static_cast<double>(w.b3[n]) + sum);
+        v = static_cast<float>(sc3 * (static_cast<double>(w.b3[n]) + sum));
       }
       uint32_t bits;
       std::memcpy(&bits, &v, 4);
       put(L::B3 + c, lane, bits);
+    }
+    {
+      const float inv = static_cast<float>(std::ldexp(1.0, -s3));
+      uint32_t bits;
+      std::memcpy(&bits, &inv, 4);
+      put(L::SC, lane, bits);
     }
   }
   return f;
@@ -172,15 +188,14 @@ struct Handle final : HandleBase {
   std::string variant_name() const override {
     char buf[160];
     if (use_tc && tc_detail::g_tc_last_pair)
-      std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, merge + epilogue kernels)",
-                    H, cfg.noise_mode, n_chunks);
+      std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
+                    H, cfg.noise_mode, n_chunks, n_groups);
     else if (use_tc)
-      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=%d,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %s)",
-                    H, tc_mt, cfg.noise_mode, chunk_samples, n_chunks,
-                    coop_tail() ? "cooperative merge+epilogue" : "merge + epilogue kernels");
+      std::snprintf(buf, sizeof(buf), "rollout_tc_kernel<f32,H=%d,MT=%d,noise=%d> (mma.sync f16x3, chunk %d, %d chunks, %d groups, group merge + tail kernels)",
+                    H, tc_mt, cfg.noise_mode, chunk_samples, n_chunks, n_groups);
     else if (use_ws)
-      std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks%s)", H, ws_L,
-                    cfg.noise_mode, ws_smem_w ? "smem-weights" : "const-weights", n_chunks, merge_G ? ", pre-merged" : "");
+      std::snprintf(buf, sizeof(buf), "rollout_ws_kernel<f32,H=%d,L=%d,noise=%d,%s> (chunk 32, %d chunks, %d groups)", H, ws_L,
+                    cfg.noise_mode, ws_smem_w ? "smem-weights" : "const-weights", n_chunks, n_groups);
     else
       std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
                     std::is_same<R, double>::value ? "f64" : "f32", H,
@@ -192,7 +207,11 @@ struct Handle final : HandleBase {
 
   mppi_gpu_config cfg{};
   int K = 0, T = 0, C = 1, H = 32, device = 0;
-  int n_chunks = 0, chunks_per_rank = 0, chunk_lo = 0, chunk_hi = 0;
+  // chunks of chunk_samples samples; fixed groups of chunks (group.cuh), the
+  // unit of the multi-rank exchange; this rank's groups [group_lo, group_hi)
+  // = chunks [chunk_lo, chunk_hi)
+  int n_chunks = 0, chunk_lo = 0, chunk_hi = 0;
+  int n_groups = 0, group_lo = 0, group_hi = 0;
   // K1 variant: warp-specialised fp32 kernel (chunk = 32 samples, L warps per
   // chunk) for the vehicle model, generic one-sample-per-thread kernel
   // (chunk = kBlock) otherwise.
@@ -203,16 +222,15 @@ struct Handle final : HandleBase {
   bool use_tc = false;
   int tc_mt = 2;
   DevBuf<uint32_t> d_tcfrag;
-  // tensor-core tail (tail.cuh): element-parallel merge into one row per
-  // controller, cooperative inside K1 when the grid is one wave
-  DevBuf<Acc> d_merged;
-  DevBuf<unsigned> d_tail_cnt;
+  // tensor-core tail (tail.cuh): merge of the group rows + epilogue, one CTA per controller
   DevBuf<unsigned char> d_plantw;  // MlpParams<float, H> (the plant step of the tail)
-  int coop_state = 0;  // 1: the cooperative K1 fits (one controller, one wave)
   int graph_kernels[4] = {0, 0, 0, 0};
-  int merge_G = 0, n_merged = 0;  // optional pre-merge of chunk partials
   bool status_direct = false;      // capture in progress: the tail writes h_status itself
-  int rank = 0, world = 1;
+  // sample sharding: NCCL all-gather of the group rows, or (in one process)
+  // peer copies from the other handles of a local group
+  enum { kExNone = 0, kExNccl = 1, kExLocal = 2 };
+  int rank = 0, world = 1, exchange_mode = kExNone;
+  std::vector<Handle<R>*> local_peers;
   int zero_start = 0;
   int partial_stride = 0;
   long long partials_ctrl_stride = 0;
@@ -231,7 +249,7 @@ struct Handle final : HandleBase {
 
   // device state
   DevBuf<R> d_plan, d_x0, d_inj, d_decay;
-  DevBuf<Acc> d_costs, d_partials, d_partials2, d_agg, d_w, d_rho_eta;
+  DevBuf<Acc> d_costs, d_partials, d_groups, d_agg, d_w, d_rho_eta;
   DevBuf<R> d_states, d_utrace, d_xtrace;
   DevBuf<double> d_eps_ref;
   DevBuf<uint64_t> d_iters, d_seeds, d_trace_base;
@@ -253,9 +271,9 @@ struct Handle final : HandleBase {
 
   // profiling
   bool profile = false;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_it0 = nullptr, ev_it1 = nullptr;
-  double prof_ms = 0;
-  uint64_t prof_launches = 0;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_it0 = nullptr, ev_it1 = nullptr, ev_x0 = nullptr, ev_x1 = nullptr;
+  double prof_ms = 0, prof_x_ms = 0;
+  uint64_t prof_launches = 0, prof_x_n = 0;
 
   // graphs: 0 = step (compute+slide), 1 = compute only, 2 = closed-loop iteration
   cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -281,11 +299,15 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaEventCreate(&ev_b));
     CUDA_TRY(cudaEventCreate(&ev_it0));
     CUDA_TRY(cudaEventCreate(&ev_it1));
+    CUDA_TRY(cudaEventCreate(&ev_x0));
+    CUDA_TRY(cudaEventCreate(&ev_x1));
     choose_variant();
     n_chunks = (K + chunk_samples - 1) / chunk_samples;
-    chunks_per_rank = n_chunks;
     chunk_lo = 0;
     chunk_hi = n_chunks;
+    n_groups = group_count(n_chunks);
+    group_lo = 0;
+    group_hi = n_groups;
     zero_start = K - static_cast<int>(std::lround(c.explore_fraction * K));
     partial_stride = kPartialHeader + 2 * T;
     partials_ctrl_stride = static_cast<long long>(n_chunks) * partial_stride;
@@ -298,8 +320,7 @@ struct Handle final : HandleBase {
     d_costs.alloc(static_cast<size_t>(C) * K);
     if (c.weight_rule == MPPI_WEIGHT_CEM) d_w.alloc(K);  // (allocated before any graph capture)
     d_partials.alloc(static_cast<size_t>(C) * partials_ctrl_stride);
-    setup_merge();
-    setup_tail();
+    d_groups.alloc(static_cast<size_t>(C) * n_groups * partial_stride);
     d_agg.alloc(static_cast<size_t>(2) * T);
     d_iters.alloc(C);
     CUDA_TRY(cudaMemset(d_iters.p, 0, C * sizeof(uint64_t)));
@@ -307,7 +328,9 @@ struct Handle final : HandleBase {
     d_trace_base.alloc(C);
     d_seeds.alloc(C);
     std::vector<uint64_t> seeds(C);
-    for (int i = 0; i < C; ++i) seeds[i] = c.seed + static_cast<uint64_t>(i);
+    // keyed by the GLOBAL controller index (a fleet sharded over ranks keeps
+    // one noise stream per controller whatever the rank count)
+    for (int i = 0; i < C; ++i) seeds[i] = c.seed + static_cast<uint64_t>(c.controller_offset) + static_cast<uint64_t>(i);
     CUDA_TRY(cudaMemcpy(d_seeds.p, seeds.data(), C * sizeof(uint64_t), cudaMemcpyHostToDevice));
     d_abort.alloc(C);
     CUDA_TRY(cudaMemset(d_abort.p, 0, C * sizeof(int)));
@@ -336,6 +359,9 @@ struct Handle final : HandleBase {
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
     if (comm) nccl().CommDestroy(comm);
+    leave_local_group();
+    if (ev_x0) cudaEventDestroy(ev_x0);
+    if (ev_x1) cudaEventDestroy(ev_x1);
     if (ev_a) cudaEventDestroy(ev_a);
     if (ev_b) cudaEventDestroy(ev_b);
     if (ev_it0) cudaEventDestroy(ev_it0);
@@ -383,41 +409,6 @@ struct Handle final : HandleBase {
     if (H == 64 && L < 2) L = 2;
     ws_L = L;
   }
-  void setup_merge() {
-    merge_G = 0;
-    n_merged = n_chunks;
-    // pre-merge groups of up to 32 chunks (each staged in shared memory,
-    // <= ~160 KB) whenever the epilogue would otherwise walk > 2 tiles
-    // (tensor-core path: above 1024 chunks, where the element-parallel tail's
-    // per-thread row walk outgrows the extra launch: c2 -27 us, K=262144
-    // -57 us per iteration; at c1's 1024 it does not pay)
-    int tc_min = 1024;
-    if (const char* e = std::getenv("MPPI_PREMERGE_MIN")) tc_min = std::atoi(e);
-    if ((!use_tc && n_chunks > 64) || (use_tc && n_chunks > tc_min)) {
-      merge_G = std::max(1, std::min(32, static_cast<int>((160 * 1024) / (8 * partial_stride))));
-      n_merged = (n_chunks + merge_G - 1) / merge_G;
-      d_partials2.alloc(static_cast<size_t>(C) * n_merged * partial_stride);
-    }
-  }
-
-  void setup_tail() {
-    coop_state = 0;
-    if (!use_tc) return;
-    d_merged.alloc(static_cast<size_t>(C) * partial_stride);
-    d_tail_cnt.alloc(C);
-    CUDA_TRY(cudaMemset(d_tail_cnt.p, 0, C * sizeof(unsigned)));
-    // The cooperative tail is opt-in (MPPI_TAIL=coop): measured slower than the
-    // separate merge + epilogue kernels on B200 (profiles/README.md).
-    const char* e = std::getenv("MPPI_TAIL");
-    const bool wanted = e && std::string(e) == "coop";
-    if (C == 1 && wanted &&
-        (H == 32 ? tc_coop_fits<32>(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 32>(T, 1, 1, partial_stride, true))
-                 : tc_coop_fits<64>(T, tc_mt, n_chunks, epilogue_smem_bytes<float, 64>(T, 1, 1, partial_stride, true))))
-      coop_state = 1;
-  }
-  // MPPI_TAIL=kernels forces the separate merge + epilogue kernels.
-  bool coop_tail() const { return use_tc && world == 1 && C == 1 && coop_state == 1; }
-
   static void validate_config(const mppi_gpu_config& c) {
     // SamplingParams::validate (types.hpp:105-122)
     if (c.samples < 1) throw_invalid("SamplingParams: samples must be >= 1");
@@ -452,6 +443,7 @@ struct Handle final : HandleBase {
       throw_invalid("system");
     if (c.mlp_hidden != 32 && c.mlp_hidden != 64) throw_invalid("mlp_hidden must be 32 or 64");
     if (c.n_controllers < 1) throw_invalid("n_controllers must be >= 1");
+    if (c.controller_offset < 0) throw_invalid("controller_offset must be >= 0");
     if (c.noise_mode == MPPI_NOISE_INJECTED && c.n_controllers != 1)
       throw Error(MPPI_ERR_UNSUPPORTED, "injected noise supports one controller per handle");
     if (c.horizon_steps > 4096) throw Error(MPPI_ERR_UNSUPPORTED, "horizon_steps > 4096");
@@ -583,7 +575,9 @@ struct Handle final : HandleBase {
     for (int c = 0; c < C; ++c) {
       d_map_fleet[c] = std::make_unique<DevBuf<R>>();
       d_map_fleet[c]->alloc(n);
-      perturb_map_kernel<R><<<592, 256, 0, stream>>>(d_map_shared.p, n, c, sigma, seed, d_map_fleet[c]->p);
+      // (stream of the GLOBAL controller index, as the noise seeds)
+      perturb_map_kernel<R><<<592, 256, 0, stream>>>(d_map_shared.p, n, c + cfg.controller_offset, sigma, seed,
+                                                     d_map_fleet[c]->p);
       ++launches;
       CUDA_TRY(cudaGetLastError());
       ptrs[c] = d_map_fleet[c]->p;
@@ -758,19 +752,19 @@ struct Handle final : HandleBase {
 
   // events: bracket the launch with ev_a/ev_b without synchronising (used
   // inside captured graphs; the caller reads the elapsed time afterwards).
-  void enqueue_rollout(int mode, bool events = false, const TailArgs* tail = nullptr) {
+  void enqueue_rollout(int mode, bool events = false) {
     const RolloutArgs<R> a = rollout_args();
-    const TailArgs no_tail{};
     const size_t smem = rollout_smem();
     const dim3 grid(chunk_hi - chunk_lo, C);
+    if (chunk_hi <= chunk_lo) return;  // a rank without samples (fewer chunks than ranks)
     // inside stream capture an event record is only a dependency edge unless
     // it is marked external; external records become graph event nodes
     if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_a, stream, cudaEventRecordExternal));
     else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
     if (use_tc) {
       if constexpr (std::is_same<R, float>::value)
-        CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(
-            a, d_tcfrag.p, tail ? *tail : no_tail, mode, tc_mt, chunk_hi - chunk_lo, C, stream));
+        CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, mode, tc_mt,
+                                                                          chunk_hi - chunk_lo, C, stream));
     } else if (use_ws) {
       launch_ws(a, mode, grid);
     } else {
@@ -794,25 +788,20 @@ struct Handle final : HandleBase {
     }
   }
 
-  void enqueue_premerge() {
-    if (!merge_G) return;
-    const dim3 grid(n_merged, C);
-    const size_t smem = sizeof(Acc) * (static_cast<size_t>(merge_G) * partial_stride + merge_G);
-    if (smem > 48 * 1024)
-      CUDA_TRY(cudaFuncSetAttribute(merge_chunks_kernel<>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    merge_chunks_kernel<><<<grid, 512, smem, stream>>>(d_partials.p, n_chunks, partial_stride, partials_ctrl_stride,
-                                                   merge_G, cfg.lambda, d_partials2.p,
-                                                   static_cast<long long>(n_merged) * partial_stride);
+  // The fixed-group merge of this rank's chunk partials (group.cuh);
+  // programmatic dependent of K1 when K1 ran just before it.
+  void enqueue_group_merge(bool after_k1) {
+    CUDA_TRY(launch_group_merge(d_partials.p, partials_ctrl_stride, n_chunks, n_groups, group_lo, group_hi - group_lo,
+                                partial_stride, cfg.lambda, d_groups.p,
+                                static_cast<long long>(n_groups) * partial_stride, C, after_k1, stream));
     ++launches;
-    CUDA_TRY(cudaGetLastError());
   }
 
-  // One iteration after the host inputs are staged.  Tensor-core path: the
-  // cooperative K1 (rollout + merge + epilogue, one launch), or K1, [the
-  // all-gather of chunk partials], the element-parallel merge and the
-  // epilogue over the merged row — identical arithmetic either way.  Other
-  // K1 variants: K1, exchange, pre-merge, epilogue.
+  // One iteration after the host inputs are staged: K1 over this rank's
+  // chunks, the fixed-group merge, [the exchange of group rows], then the
+  // merge of the group rows + epilogue (tensor-core path: tail_kernel;
+  // otherwise epilogue_kernel).  CEM: K1, the elite selection, the weighted
+  // average over the regenerated batch, the epilogue.
   void enqueue_iteration(int mode, bool events, bool slide, bool increment, bool plant, bool trace) {
     if (cfg.weight_rule == MPPI_WEIGHT_CEM) {
       // CEM (controller.cpp:111-116 -> weights.cpp:27-53): K1 for the costs,
@@ -835,57 +824,68 @@ struct Handle final : HandleBase {
       enqueue_epilogue(false, slide, increment, plant, trace, 1);
       return;
     }
+    enqueue_front(mode, events);
+    enqueue_back(events, slide, increment, plant, trace);
+  }
+  // K1 + the group merge (everything before the exchange).  (With K1's event
+  // nodes around it, the group merge is an ordinary dependent.)
+  void enqueue_front(int mode, bool events) {
+    const bool k1 = chunk_hi > chunk_lo;
+    enqueue_rollout(mode, events);
+    enqueue_group_merge(k1 && !events);
+  }
+  // the exchange, the merge of the group rows and the epilogue
+  void enqueue_back(bool events, bool slide, bool increment, bool plant, bool trace) {
+    enqueue_exchange(events);
     if (use_tc) {
-      if constexpr (std::is_same<R, float>::value) {
-        if (coop_tail()) {
-          TailArgs ta{};
-          ta.mode = 1;
-          ta.merged = d_merged.p;
-          ta.plant_w = d_plantw.p;
-          ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
-          enqueue_rollout(mode, events, &ta);
-          return;
-        }
-      }
-      enqueue_rollout(mode, events);
-      enqueue_exchange();
       if constexpr (std::is_same<R, float>::value) {
         TailArgs ta{};
         ta.plant_w = d_plantw.p;
         ta.e = epilogue_args(true, slide, increment, plant, trace, /*merged_row=*/true);
         if (status_direct) ta.e.status_host = h_status.p;  // mapped pinned (UVA)
-        enqueue_premerge();
-        const Acc* rows = merge_G ? d_partials2.p : d_partials.p;
-        const int n_rows = merge_G ? n_merged : n_chunks;
-        const long long rows_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
-        CUDA_TRY((H == 32 ? launch_tail_tc<32> : launch_tail_tc<64>)(rows, n_rows, partial_stride, rows_stride,
-                                                                      cfg.lambda, d_merged.p, d_tail_cnt.p, ta, C, stream));
+        // a programmatic dependent of the group merge unless the exchange sits between
+        const bool pdl = world == 1;
+        CUDA_TRY((H == 32 ? launch_tail_tc<32> : launch_tail_tc<64>)(
+            d_groups.p, n_groups, partial_stride, static_cast<long long>(n_groups) * partial_stride, cfg.lambda, ta,
+            C, pdl, stream));
         ++launches;
       }
       return;
     }
-    enqueue_rollout(mode, events);
-    enqueue_exchange();
-    enqueue_premerge();
     enqueue_epilogue(true, slide, increment, plant, trace, C);
   }
 
-  void enqueue_exchange() {
+  // The exchange of the group rows: rank r's rows [group_lo, group_hi) to
+  // every rank (NCCL all-gather in place, or peer copies in a local group).
+  void enqueue_exchange(bool events) {
     if (world <= 1) return;
-    const size_t count = static_cast<size_t>(chunks_per_rank) * partial_stride;
-    Acc* base = d_partials.p;
-    NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, ncclFloat64, comm, stream));
+    const size_t count = static_cast<size_t>(n_groups / world) * partial_stride;
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_x0, stream, cudaEventRecordExternal));
+    if (exchange_mode == kExNccl) {
+      Acc* base = d_groups.p;
+      NCCL_TRY(nccl().AllGather(base + static_cast<size_t>(rank) * count, base, count, ncclFloat64, comm, stream));
+    } else if (exchange_mode == kExLocal) {
+      for (int p = 0; p < world; ++p) {
+        if (p == rank) continue;
+        const Handle<R>* peer = local_peers[p];
+        if (!peer) throw Error(MPPI_ERR_RUNTIME, "local group: a peer handle was destroyed");
+        CUDA_TRY(cudaMemcpyPeerAsync(d_groups.p + static_cast<size_t>(p) * count, device,
+                                     peer->d_groups.p + static_cast<size_t>(p) * count, peer->device,
+                                     count * sizeof(Acc), stream));
+      }
+    }
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_x1, stream, cudaEventRecordExternal));
   }
 
   EpilogueArgs<R> epilogue_args(bool merge, bool slide, bool increment, bool plant, bool trace,
                                 bool merged_row = false) const {
     EpilogueArgs<R> e{};
     e.T = T;
-    e.n_chunks = merge_G ? n_merged : n_chunks;
+    e.n_chunks = n_groups;  // the rows merged by the epilogue: the group rows
     // rows per shared-memory tile: <= 32 and <= ~96 KB
     e.tile_rows = std::max(1, std::min({32, e.n_chunks, static_cast<int>((96 * 1024) / (8 * partial_stride))}));
     e.partial_stride = partial_stride;
-    e.partials_ctrl_stride = merge_G ? static_cast<long long>(n_merged) * partial_stride : partials_ctrl_stride;
+    e.partials_ctrl_stride = static_cast<long long>(n_groups) * partial_stride;
     e.lambda = cfg.lambda;
     e.lo0 = static_cast<R>(cfg.bounds_lower[0]);
     e.lo1 = static_cast<R>(cfg.bounds_lower[1]);
@@ -896,9 +896,9 @@ struct Handle final : HandleBase {
     e.slide = slide;
     e.increment = increment;
     e.plant = plant;
-    e.partials = merge ? (merge_G ? d_partials2.p : d_partials.p) : nullptr;
-    if (merge && merged_row) {  // the tensor-core path's single merged row (tail.cuh)
-      e.partials = d_merged.p;
+    e.partials = merge ? d_groups.p : nullptr;
+    if (merge && merged_row) {  // the tensor-core tail merges in shared memory (tail.cuh)
+      e.partials = nullptr;
       e.n_chunks = 1;
       e.tile_rows = 1;
       e.partials_ctrl_stride = partial_stride;
@@ -960,8 +960,7 @@ struct Handle final : HandleBase {
         n_before_capture = launches;
         // step graphs on the tensor-core path: the tail writes the host status
         // mirror itself (no device-to-host copy node at the end of the graph)
-        status_direct = which < 2 && use_tc && !coop_tail() && std::is_same<R, float>::value &&
-                        cfg.weight_rule != MPPI_WEIGHT_CEM;
+        status_direct = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
         enqueue_iteration(cfg.noise_mode, /*events=*/which == 2, slide, /*increment=*/slide, plant, trace);
         profile = prof;
         const bool direct = status_direct;
@@ -1052,7 +1051,7 @@ struct Handle final : HandleBase {
   }
 
   void closed_loop(const double* x_init, int iterations, double* u_trace, double* x_trace,
-                   size_t flush_bytes, double* ms_out) {
+                   size_t flush_bytes, double* ms_out, double* iter_ms_out) {
     if (iterations < 1) throw_invalid("closed_loop: iterations must be >= 1");
     require_ready();
     upload_x0(x_init);
@@ -1093,10 +1092,18 @@ struct Handle final : HandleBase {
         float ms = 0;
         CUDA_TRY(cudaEventElapsedTime(&ms, ev_it0, ev_it1));
         total += ms;
+        if (iter_ms_out) iter_ms_out[i] = ms;
         float k1 = 0;
-        if (k1_events && cudaEventElapsedTime(&k1, ev_a, ev_b) == cudaSuccess) {
+        if (k1_events && chunk_hi > chunk_lo && cudaEventElapsedTime(&k1, ev_a, ev_b) == cudaSuccess) {
           prof_ms += k1;
           ++prof_launches;
+        } else {
+          cudaGetLastError();
+        }
+        float xm = 0;
+        if (k1_events && world > 1 && cudaEventElapsedTime(&xm, ev_x0, ev_x1) == cudaSuccess) {
+          prof_x_ms += xm;
+          ++prof_x_n;
         } else {
           cudaGetLastError();
         }
@@ -1165,8 +1172,7 @@ struct Handle final : HandleBase {
     CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
     CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
     const int mode = effective_mode(eps_in != nullptr);
-    enqueue_rollout(mode);
-    enqueue_exchange();
+    enqueue_rollout(mode);  // (this rank's samples only when sharded)
     CUDA_TRY(cudaMemcpyAsync(costs_out, d_costs.p, K * sizeof(Acc), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
     batch_valid = true;
@@ -1265,8 +1271,8 @@ struct Handle final : HandleBase {
       CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
       if (use_tc) {
         if constexpr (std::is_same<R, float>::value)
-          CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(
-              a, d_tcfrag.p, TailArgs{}, effective_mode(batch_injected), tc_mt, n_chunks, 1, stream));
+          CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, effective_mode(batch_injected),
+                                                                            tc_mt, n_chunks, 1, stream));
       } else {
         launch_ws(a, effective_mode(batch_injected), dim3(n_chunks, 1));
       }
@@ -1285,32 +1291,118 @@ struct Handle final : HandleBase {
   }
 
   // ----------------------------------------------------------- multi-GPU --
-  void set_comm(int r, int w, const unsigned char id[128]) {
+  // Validation first, then the commit: a rejected call leaves the handle as it was.
+  void validate_shard(int r, int w) const {
     if (w < 1 || r < 0 || r >= w) throw_invalid("set_comm: bad rank/world_size");
-    if (C != 1) throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: fleets shard controllers, not samples");
+    if (w > 1 && C != 1) throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: fleets shard controllers, not samples");
     if (cfg.weight_rule == MPPI_WEIGHT_CEM && w > 1)
       throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: the CEM rule needs every cost on one device");
+    if (n_groups % w != 0)
+      throw Error(MPPI_ERR_UNSUPPORTED, "set_comm: world_size must divide the exchange group count (" +
+                                            std::to_string(n_groups) + ")");
+  }
+  void apply_shard(int r, int w, int mode) {
+    rank = r;
+    world = w;
+    exchange_mode = w > 1 ? mode : static_cast<int>(kExNone);
+    group_lo = r * (n_groups / w);
+    group_hi = (r + 1) * (n_groups / w);
+    chunk_lo = group_first_chunk(group_lo, n_chunks, n_groups);
+    chunk_hi = group_first_chunk(group_hi, n_chunks, n_groups);
+    invalidate_graphs();
+  }
+  void set_comm(int r, int w, const unsigned char id[128]) override {
+    validate_shard(r, w);
+    ncclComm_t fresh = nullptr;
+    if (w > 1) {
+      if (!id) throw_invalid("set_comm: null id");
+      ncclUniqueId uid;
+      static_assert(sizeof(uid) == 128, "ncclUniqueId must be 128 bytes");
+      std::memcpy(&uid, id, 128);
+      NCCL_TRY(nccl().CommInitRank(&fresh, w, uid, r));
+    }
+    if (comm) nccl().CommDestroy(comm);
+    comm = fresh;
+    leave_local_group();
+    apply_shard(r, w, kExNccl);
+  }
+  // In-process sharding over `peers` (this handle is peers[r]): the exchange
+  // copies the other ranks' group rows from their buffers.
+  void set_comm_local_base(const std::vector<HandleBase*>& base, int r) override {
+    std::vector<Handle<R>*> peers;
+    for (HandleBase* b : base) {
+      auto* p = dynamic_cast<Handle<R>*>(b);
+      if (!p) throw_invalid("set_comm_local: every handle of a group needs the same precision");
+      peers.push_back(p);
+    }
+    set_comm_local(peers, r);
+  }
+  void set_comm_local(const std::vector<Handle<R>*>& peers, int r) {
+    const int w = static_cast<int>(peers.size());
+    validate_shard(r, w);
+    for (const Handle<R>* p : peers) {
+      if (!p) throw_invalid("set_comm_local: null handle");
+      if (p->K != K || p->T != T || p->H != H || p->C != C || p->n_chunks != n_chunks || p->n_groups != n_groups ||
+          p->cfg.seed != cfg.seed || p->cfg.noise_mode != cfg.noise_mode || p->cfg.system != cfg.system)
+        throw_invalid("set_comm_local: every handle of a group needs the same configuration");
+    }
+    for (const Handle<R>* p : peers)
+      if (p->device != device) {
+        cudaDeviceEnablePeerAccess(p->device, 0);  // best effort: the copies stage through the host otherwise
+        cudaGetLastError();
+      }
     if (comm) {
       nccl().CommDestroy(comm);
       comm = nullptr;
     }
-    rank = r;
-    world = w;
-    chunks_per_rank = (n_chunks + w - 1) / w;
-    chunk_lo = std::min(n_chunks, r * chunks_per_rank);
-    chunk_hi = std::min(n_chunks, (r + 1) * chunks_per_rank);
-    if (chunk_hi <= chunk_lo) throw_invalid("set_comm: more ranks than sample chunks");
-    partials_ctrl_stride = static_cast<long long>(w) * chunks_per_rank * partial_stride;
-    d_partials.alloc(static_cast<size_t>(partials_ctrl_stride));
-    setup_merge();
-    setup_tail();
-    if (w > 1) {
-      ncclUniqueId uid;
-      static_assert(sizeof(uid) == 128, "ncclUniqueId must be 128 bytes");
-      std::memcpy(&uid, id, 128);
-      NCCL_TRY(nccl().CommInitRank(&comm, w, uid, r));
+    leave_local_group();
+    local_peers = peers;
+    apply_shard(r, w, kExLocal);
+  }
+  void leave_local_group() {
+    for (Handle<R>* p : local_peers)
+      if (p && p != this)
+        for (auto& q : p->local_peers)
+          if (q == this) q = nullptr;
+    local_peers.clear();
+  }
+  // A step of a local group in phases, driven by mppi_gpu_step_local
+  // (abi.cpp): every rank's front (K1 + group merge), a host sync, then every
+  // rank's back (exchange + tail) — no kernel ever waits on another rank's.
+  void local_front(const double* x0) override {
+    require_ready();
+    if (exchange_mode != kExLocal) throw_invalid("step_local: handle is not in a local group");
+    upload_x0(x0);
+    CUDA_TRY(cudaMemsetAsync(d_status.p, 0, C * sizeof(StepStatus), stream));
+    CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+    enqueue_front(cfg.noise_mode, false);
+  }
+  void local_back(bool slide) override {
+    enqueue_back(/*events=*/false, slide, /*increment=*/slide, false, false);
+    CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
+  }
+  void local_finish(double* u0) override {
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const int code = check_status(true);
+    if (code != MPPI_OK) throw_status(code);
+    if (u0)
+      for (int c = 0; c < C; ++c) {
+        u0[c * 2] = h_status.p[c].u0[0];
+        u0[c * 2 + 1] = h_status.p[c].u0[1];
+      }
+  }
+  void sync_stream() override { CUDA_TRY(cudaStreamSynchronize(stream)); }
+  void shard_info(int* out) const override {
+    const int v[8] = {rank, world, n_chunks, n_groups, chunk_lo, chunk_hi, group_lo, group_hi};
+    for (int i = 0; i < 8; ++i) out[i] = v[i];
+  }
+  void read_exchange_profile(double* ms, uint64_t* n, bool reset) override {
+    if (ms) *ms = prof_x_ms;
+    if (n) *n = prof_x_n;
+    if (reset) {
+      prof_x_ms = 0;
+      prof_x_n = 0;
     }
-    invalidate_graphs();
   }
 };
 

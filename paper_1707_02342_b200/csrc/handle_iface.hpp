@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/mppi_gpu.h"
 
@@ -31,7 +32,7 @@ struct HandleBase {
   virtual void slide_only() = 0;
   virtual void optimize(const double* x0, int iterations) = 0;
   virtual void closed_loop(const double* x_init, int iterations, double* u_trace, double* x_trace,
-                           size_t flush_bytes, double* ms_out) = 0;
+                           size_t flush_bytes, double* ms_out, double* iter_ms_out) = 0;
   virtual void sample_perturbations(uint64_t iteration, double* eps_out, uint8_t* flags_out) = 0;
   virtual void rollout_costs(const double* x0, const double* eps_in, double* costs_out,
                              double* eps_stored_out) = 0;
@@ -39,6 +40,13 @@ struct HandleBase {
   virtual void update_plan(const double* w) = 0;
   virtual void rollout_states(const double* x0, int sample, double* out) = 0;
   virtual void set_comm(int rank, int world, const unsigned char id[128]) = 0;
+  virtual void set_comm_local_base(const std::vector<HandleBase*>& peers, int rank) = 0;
+  virtual void local_front(const double* x0) = 0;
+  virtual void local_back(bool slide) = 0;
+  virtual void local_finish(double* u0) = 0;
+  virtual void sync_stream() = 0;
+  virtual void shard_info(int* out) const = 0;
+  virtual void read_exchange_profile(double* ms, uint64_t* n, bool reset) = 0;
   virtual void* stream_ptr() const = 0;
   virtual uint64_t launch_count() const = 0;
   virtual void set_profile(bool on) = 0;

@@ -10,8 +10,9 @@
 // as rollout_batch leaves it (eps - U for zero-mean samples,
 // controller.cpp:70-72).  eps' is REGENERATED from the counters for the
 // numerator, so the K x T x 2 batch never touches HBM.  The per-chunk
-// partials are merged in fixed global chunk order by K2 (epilogue.cuh), which
-// makes the result independent of the GPU count and of scheduling.
+// partials are merged into fixed groups (group.cuh) and the group rows in
+// group order by K2 (epilogue.cuh), which makes the result independent of the
+// GPU count and of scheduling.
 #pragma once
 
 #include "model.cuh"
@@ -332,56 +333,6 @@ __global__ void inject_transpose_kernel(const double* __restrict__ ref, int K, i
     const int t = static_cast<int>(i / K);
     dev[i * 2] = static_cast<R>(ref[(static_cast<size_t>(k) * 2) * T + t]);
     dev[i * 2 + 1] = static_cast<R>(ref[(static_cast<size_t>(k) * 2 + 1) * T + t]);
-  }
-}
-
-// Pre-merge of G consecutive chunk partials into one (same format), in fixed
-// order, when a launch produced many small chunks.  grid = (ceil(n_in / G), C).
-// All G x stride values are loaded at once (one L2 round trip: thread t takes
-// flat indices t, t + blockDim, ...), scaled by their chunk factor into shared
-// memory, then summed per element over the chunks in ascending order.
-// Dynamic smem: G x stride doubles + G doubles.
-template <int kUnused = 0>
-__global__ void merge_chunks_kernel(const Acc* __restrict__ in, int n_in, int stride, long long in_ctrl_stride,
-                                    int G, double lambda, Acc* __restrict__ out, long long out_ctrl_stride) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Acc* s_val = reinterpret_cast<Acc*>(smem_raw);  // [G][stride]
-  Acc* s_scale = s_val + static_cast<size_t>(G) * stride;
-  __shared__ Acc s_red[32];
-  __shared__ int s_bad;
-  const int b = blockIdx.x, ctrl = blockIdx.y;
-  const int c0 = b * G, c1 = min(n_in, c0 + G), n = c1 - c0;
-  const Acc* P = in + static_cast<size_t>(ctrl) * in_ctrl_stride + static_cast<size_t>(c0) * stride;
-  if (threadIdx.x == 0) s_bad = 0;
-  const int total = n * stride;
-  for (int f = threadIdx.x; f < total; f += blockDim.x) s_val[f] = P[f];
-  __syncthreads();
-  Acc m = INFINITY;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const Acc r = s_val[c * stride];
-    m = (r < m) ? r : m;
-    if (s_val[c * stride + 2] != 0.0) s_bad = 1;
-  }
-  m = warp_min(m);
-  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  Acc rho = s_red[0];
-  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) rho = (s_red[w] < rho) ? s_red[w] : rho;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) s_scale[c] = exp(-(s_val[c * stride] - rho) / lambda);
-  __syncthreads();
-  Acc* o = out + static_cast<size_t>(ctrl) * out_ctrl_stride + static_cast<size_t>(b) * stride;
-  for (int i = threadIdx.x; i < stride; i += blockDim.x) {
-    if (i == 0) {
-      o[0] = rho;
-    } else if (i == 2) {
-      o[2] = s_bad ? 1.0 : 0.0;
-    } else if (i == 3) {
-      o[3] = 0.0;
-    } else {
-      Acc sum = 0.0;
-      for (int c = 0; c < n; ++c) sum = fma(s_scale[c], s_val[c * stride + i], sum);
-      o[i] = sum;
-    }
   }
 }
 

@@ -46,16 +46,26 @@ namespace mppi_dev {
 //   W3 .. : B3 (k16 x n8, outputs 0..3): W3 + (kk*2 + r)*2 + hl
 //   B2 .. : bias2 (fp32 bits): B2 + j*2 + c, column 8j + 2t + c
 //   B3 .. : bias3 (fp32 bits): column 2t + c (zero for t >= 2)
+//   SC    : 2^-s (fp32 bits, every lane): layer 3 runs on 2^s-scaled weights
 // H = 32 keeps every fragment in registers; at H = 64 the 128 layer-2 words
 // live in shared memory (one LDS.128 per (kk, j), shared by the CTA's warps).
+//
+// Layer-3 scaling: 2 W3 (~0.08 for the BASELINE Xavier x 0.1 output layer)
+// would leave the lo halves of its fp16 split (~4e-5) in the fp16 subnormal
+// range below 6.1e-5, which keeps ~2^-24 absolute, not 11 significant bits:
+// the output layer would carry ~10x the rounding of an fp32 evaluation.  The
+// host scales W3 and its bias by the power of two s that brings max |2 W3|
+// into [0.5, 1) (tc_build_fragments), which is exact, and the kernel folds
+// 2^-s into the dt of the dynamic block: RN(d 2^s * dt 2^-s) = RN(d dt).
 template <int H>
 struct TcLayout {
   static constexpr int NJ = H / 8, NK = H / 16;
   static constexpr int W1 = 0, W2 = 2 * NJ, W3 = W2 + 4 * NK * NJ, B2 = W3 + 4 * NK, B3 = B2 + 2 * NJ;
-  static constexpr int WORDS = B3 + 2;
+  static constexpr int SC = B3 + 2;
+  static constexpr int WORDS = SC + 1;
   static constexpr bool W2_SMEM = H > 32;
 };
-constexpr int kTcWords = TcLayout<32>::WORDS;  // 58
+constexpr int kTcWords = TcLayout<32>::WORDS;  // 59
 constexpr int kTcH = 32;
 
 __device__ __forceinline__ void mma_k8(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
@@ -336,10 +346,8 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
 // numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
 template <int H, int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
 __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
-                                                            const uint32_t* __restrict__ frag,
-                                                            const __grid_constant__ TailArgs tail) {
+                                                            const uint32_t* __restrict__ frag) {
   constexpr int CH = 16 * MT;
-  static_assert(32 * NW == kMergeBlock, "the cooperative merge must use the merge kernel's block shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
   float* s_plan = reinterpret_cast<float*>(smem_raw);
@@ -412,12 +420,13 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const bool dup = (MT == 1) && (t4 >= 2);  // MT = 1: lanes t >= 2 mirror t - 2
   const int k = chunk * CH + 16 * m_own + row_own;
   // warps past the rank's last chunk (last CTA only) run without writing
-  // anything; they stay alive for the cooperative tail's grid barriers
+  // anything (they keep the warp-synchronous code uniform)
   const bool active = chunk < a.chunk_end;
   const bool valid = (k < a.K) && !dup && active;
   const bool zm = k >= a.zero_start;
   const int kn = (k < a.K) ? k : 0;  // noise counter (in range for every lane)
   const float dt = a.sys.dt;
+  const float dt3 = dt * __uint_as_float(frag[L::SC * 32 + lane]);  // dt 2^-s (exact)
   const CostDev<float> cp = a.sys.cost;
   const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
   const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
@@ -540,10 +549,10 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     __syncwarp();
     const float4 d = st.out[m_own][row_own];
     // the dynamic block of the Euler split
-    roll = add_rn(roll, mul_rn(d.x, dt));
-    vx = add_rn(vx, mul_rn(d.y, dt));
-    vy = add_rn(vy, mul_rn(d.z, dt));
-    thd = add_rn(thd, mul_rn(d.w, dt));
+    roll = add_rn(roll, mul_rn(d.x, dt3));
+    vx = add_rn(vx, mul_rn(d.y, dt3));
+    vy = add_rn(vy, mul_rn(d.z, dt3));
+    thd = add_rn(thd, mul_rn(d.w, dt3));
     q = q_next;  // consumed by the next step's cost
     p_roll = roll;
     p_vx = vx;
@@ -586,21 +595,23 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   double* red = s_red_all + static_cast<size_t>(warp) * (2 * kTcTB) * kTcRedStride;
   if constexpr (STORE && MT == 1) {
     // eps' is on chip: each lane sums whole (t, c) elements over the chunk's
-    // rows, in the lane order of the staged reduction below (row g, then row
-    // g + 8; the mirror lanes only add zeros there), so the partials are
-    // bit-identical to it and to the warp-pair kernel's
+    // rows with the staged reduction's order below (rows 0..7 and rows 8..15
+    // as two sequential sums of rounded products, then their sum plus the
+    // mirror lanes' zero sums), so the partials are bit-identical to it and
+    // to the warp-pair kernel's: which variant a launch picks (it depends on
+    // the rank's grid size) never changes a result.
     if (!dup) red[row_own] = wk;
     __syncwarp();
     for (int e = lane; e < 2 * T; e += 32) {
       const int tt = e >> 1, c = e & 1;
-      Acc s = 0.0;
+      Acc sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const float2 ea = s_eps[tt * CH + r], eb = s_eps[tt * CH + r + 8];
-        s = s + red[r] * static_cast<Acc>(c ? ea.y : ea.x);
-        s = s + red[r + 8] * static_cast<Acc>(c ? eb.y : eb.x);
+        sa = __dadd_rn(sa, __dmul_rn(red[r], static_cast<Acc>(c ? ea.y : ea.x)));
+        sb = __dadd_rn(sb, __dmul_rn(red[r + 8], static_cast<Acc>(c ? eb.y : eb.x)));
       }
-      if (active) out[kPartialHeader + e] = s;
+      if (active) out[kPartialHeader + e] = __dadd_rn(__dadd_rn(sa, sb), 0.0);
     }
     __syncwarp();
   } else {
@@ -621,35 +632,25 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
           e1 = zm ? e1 - s_plan[2 * tt + 1] : e1;
         }
       }
-      red[(2 * j) * kTcRedStride + lane] = wk * static_cast<Acc>(e0);
-      red[(2 * j + 1) * kTcRedStride + lane] = wk * static_cast<Acc>(e1);
+      red[(2 * j) * kTcRedStride + lane] = __dmul_rn(wk, static_cast<Acc>(e0));
+      red[(2 * j + 1) * kTcRedStride + lane] = __dmul_rn(wk, static_cast<Acc>(e1));
     }
     __syncwarp();
     // four interleaved partial sums (lanes l = 4i + q), then q = 0..3: a
-    // fixed order with an 8-deep dependent chain instead of 32
+    // fixed order with an 8-deep dependent chain instead of 32.  At MT = 1
+    // q = 0 holds rows 0..7, q = 1 rows 8..15 and q = 2, 3 the mirror lanes'
+    // zeros — the order of the on-chip eps' path above.
     Acc s4[4] = {0.0, 0.0, 0.0, 0.0};
     const double* col = red + lane * kTcRedStride;
 #pragma unroll
     for (int l = 0; l < 32; l += 4) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) s4[q] = s4[q] + col[l + q];
+      for (int q = 0; q < 4; ++q) s4[q] = __dadd_rn(s4[q], col[l + q]);
     }
-    const Acc s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    const Acc s = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
     if (active && tb + (lane >> 1) < T) out[kPartialHeader + 2 * tb + lane] = s;
     __syncwarp();
   }
-  }
-  // group merge / fused epilogue (tail.cuh); the reduction buffer is scratch now
-  // cooperative tail (one controller, grid co-resident): merge of the chunk
-  // partials by all CTAs, then the epilogue by CTA 0 (tail.cuh)
-  if (tail.mode == 1) {
-    cooperative_groups::this_grid().sync();
-    merge_elements<32 * NW, false>(a.partials, a.chunk_end, a.partial_stride, a.dlambda, tail.merged, blockIdx.x,
-                                   gridDim.x, s_red_all);
-    cooperative_groups::this_grid().sync();
-    if (blockIdx.x == 0)
-      epilogue_body<float, H, VehicleMlp<float, H>, 32 * NW>(
-          tail.e, static_cast<const MlpParams<float, H>*>(tail.plant_w), 0, reinterpret_cast<unsigned char*>(s_red_all));
   }
 }
 

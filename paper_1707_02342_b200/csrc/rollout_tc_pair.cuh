@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
   const bool zm = k >= a.zero_start;
   const int kn = (k < a.K) ? k : 0;
   const float dt = a.sys.dt;
+  const float dt3 = dt * __uint_as_float(frag[L::SC * 32 + lane]);  // dt 2^-s (exact): layer 3 is 2^s-scaled
   const CostDev<float> cp = a.sys.cost;
   const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
   const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
@@ -300,10 +301,10 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
       }
       __syncwarp();
       const float4 d = st.out[row_own];
-      roll = add_rn(roll, mul_rn(d.x, dt));
-      vx = add_rn(vx, mul_rn(d.y, dt));
-      vy = add_rn(vy, mul_rn(d.z, dt));
-      thd = add_rn(thd, mul_rn(d.w, dt));
+      roll = add_rn(roll, mul_rn(d.x, dt3));
+      vx = add_rn(vx, mul_rn(d.y, dt3));
+      vy = add_rn(vy, mul_rn(d.z, dt3));
+      thd = add_rn(thd, mul_rn(d.w, dt3));
       q = q_next;
       p_roll = roll;
       p_vx = vx;
@@ -340,18 +341,20 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
     if (!dup) st.wk[row_own] = wk;
   }
   tc_pair_bar(bar_id);
-  // numerators: element e = 2t + c, sum over the rows in the single-warp
-  // kernel's lane order (row g, then row g + 8, for g = 0..7)
+  // numerators: element e = 2t + c, in the single-warp kernel's order (rows
+  // 0..7 and rows 8..15 as two sequential sums of rounded products, then
+  // their sum plus the mirror lanes' zeros), so the chunk rows are
+  // bit-identical whichever K1 variant a rank's grid size selects
   for (int e = 32 * half + lane; e < 2 * T; e += 64) {
     const int tt = e >> 1, c = e & 1;
-    Acc s = 0.0;
+    Acc sa = 0.0, sb = 0.0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const float2 ea = s_eps[tt * 16 + r], eb = s_eps[tt * 16 + r + 8];
-      s = s + st.wk[r] * static_cast<Acc>(c ? ea.y : ea.x);
-      s = s + st.wk[r + 8] * static_cast<Acc>(c ? eb.y : eb.x);
+      sa = __dadd_rn(sa, __dmul_rn(st.wk[r], static_cast<Acc>(c ? ea.y : ea.x)));
+      sb = __dadd_rn(sb, __dmul_rn(st.wk[r + 8], static_cast<Acc>(c ? eb.y : eb.x)));
     }
-    if (active) out[kPartialHeader + e] = s;
+    if (active) out[kPartialHeader + e] = __dadd_rn(__dadd_rn(sa, sb), 0.0);
   }
 }
 

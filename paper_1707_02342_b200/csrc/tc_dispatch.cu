@@ -1,10 +1,11 @@
 // tc_dispatch.cu — host dispatch of the tensor-core rollout over (H, noise
 // mode): each (H, mode) set of kernel instantiations lives in its own
 // translation unit (tc_h{32,64}_{phx,ref,inj}.cu) so they compile in
-// parallel; plus the element-parallel merge launcher.
+// parallel; plus the fixed-group merge launcher (group.cuh).
 #include <algorithm>
 
 #include "tail.cuh"
+#include "group.cuh"
 #include "ws_launch.hpp"
 
 namespace mppi_host {
@@ -14,32 +15,36 @@ int g_tc_last_pair = 0;
 }
 
 template <int H>
-cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
-                              const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
-                              cudaStream_t stream) {
+cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int mode, int mt,
+                              int n_chunks, int ctrls, cudaStream_t stream) {
   switch (mode) {
-    case mppi_dev::kInjected: return tc_detail::by_stab<H, mppi_dev::kInjected>(a, frag, tail, mt, n_chunks, ctrls, stream);
-    case mppi_dev::kRefSplitmix: return tc_detail::by_stab<H, mppi_dev::kRefSplitmix>(a, frag, tail, mt, n_chunks, ctrls, stream);
-    default: return tc_detail::by_stab<H, mppi_dev::kPhilox>(a, frag, tail, mt, n_chunks, ctrls, stream);
+    case mppi_dev::kInjected: return tc_detail::by_stab<H, mppi_dev::kInjected>(a, frag, mt, n_chunks, ctrls, stream);
+    case mppi_dev::kRefSplitmix: return tc_detail::by_stab<H, mppi_dev::kRefSplitmix>(a, frag, mt, n_chunks, ctrls, stream);
+    default: return tc_detail::by_stab<H, mppi_dev::kPhilox>(a, frag, mt, n_chunks, ctrls, stream);
   }
 }
 
-template cudaError_t launch_rollout_tc<32>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                           const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
-template cudaError_t launch_rollout_tc<64>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                           const mppi_dev::TailArgs&, int, int, int, int, cudaStream_t);
+template cudaError_t launch_rollout_tc<32>(const mppi_dev::RolloutArgs<float>&, const uint32_t*, int, int, int, int,
+                                           cudaStream_t);
+template cudaError_t launch_rollout_tc<64>(const mppi_dev::RolloutArgs<float>&, const uint32_t*, int, int, int, int,
+                                           cudaStream_t);
 
-cudaError_t launch_merge_elements(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride,
-                                  double lambda, mppi_dev::Acc* merged, int ctrls, cudaStream_t stream) {
-  const size_t smem = mppi_dev::merge_smem_bytes(n);
-  auto kern = mppi_dev::merge_elements_kernel<>;
-  if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  const dim3 grid(std::min(stride, 296), ctrls);
-  kern<<<grid, mppi_dev::kMergeBlock, smem, stream>>>(partials, n, stride, ctrl_stride, lambda, merged);
-  return cudaGetLastError();
+cudaError_t launch_group_merge(const mppi_dev::Acc* partials, long long partials_ctrl_stride, int n_chunks,
+                               int n_groups, int g0, int n_local, int stride, double lambda, mppi_dev::Acc* groups,
+                               long long groups_ctrl_stride, int ctrls, bool pdl, cudaStream_t stream) {
+  if (n_local <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_local, (stride + mppi_dev::kGroupElems - 1) / mppi_dev::kGroupElems, ctrls);
+  cfg.blockDim = dim3(mppi_dev::kGroupBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, mppi_dev::group_merge_kernel<>, partials, partials_ctrl_stride, n_chunks, n_groups,
+                            g0, stride, lambda, groups, groups_ctrl_stride);
 }
 
 }  // namespace mppi_host

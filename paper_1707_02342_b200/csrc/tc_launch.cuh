@@ -14,8 +14,8 @@ namespace tc_detail {
 constexpr int kTcWarps = 4;  // warps (chunks) per CTA
 
 template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE>
-cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
-                     int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
+cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls, size_t smem,
+                     cudaStream_t stream) {
   auto kern = mppi_dev::rollout_tc_kernel<H, MT, kTcWarps, Mode, STAB, STORE, TRACE>;
   // (static + dynamic shared memory may pass 48 KB even when `smem` does not:
   // the H = 64 kernel holds its layer-2 fragments in 16 KB of static smem)
@@ -24,31 +24,18 @@ cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
     if (e != cudaSuccess) return e;
   }
   const dim3 grid((n_chunks + kTcWarps - 1) / kTcWarps, ctrls);
-  if (tail.mode == 1) {  // cooperative: the tail's grid barriers need the whole grid co-resident
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(32 * kTcWarps);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a, frag, tail);
-  }
-  kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag, tail);
+  kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag);
   return cudaGetLastError();
 }
 // the per-step state trace (parity: mppi_gpu_rollout_states) is its own instantiation
 template <int H, int MT, int Mode, bool STAB, bool STORE>
-cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
-                     int n_chunks, int ctrls, size_t smem, cudaStream_t stream) {
+cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls, size_t smem,
+                     cudaStream_t stream) {
   // (a trace is a parity call: no on-chip eps' variant is compiled for it)
   if constexpr (!STORE) {
-    if (a.trace_states) return go_trace<H, MT, Mode, STAB, false, true>(a, frag, tail, n_chunks, ctrls, smem, stream);
+    if (a.trace_states) return go_trace<H, MT, Mode, STAB, false, true>(a, frag, n_chunks, ctrls, smem, stream);
   }
-  return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, tail, n_chunks, ctrls, smem, stream);
+  return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, n_chunks, ctrls, smem, stream);
 }
 // The warp-pair kernel (rollout_tc_pair.cuh): H = 32, eps' on chip, no trace.
 // Used by default only at no more than one chunk per SM (c0: K1 -5 %); with
@@ -89,11 +76,10 @@ cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (2 CTAs of 4 warps per SM); larger launches regenerate it from the counters.
 template <int H, int MT, int Mode, bool STAB>
-cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
-               int n_chunks, int ctrls, cudaStream_t stream) {
+cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
+               cudaStream_t stream) {
   const size_t plan_bytes = (sizeof(float) * (2 * a.T + 2) + 15) & ~size_t(15);
   const size_t base = plan_bytes + sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
-  // (the cooperative tail reuses the numerator buffers; tc_coop_fits checks they suffice)
   const size_t eps_bytes = sizeof(float2) * kTcWarps * a.T * 16 * MT;
   static int sms = [] {
     int dev = 0, n = 148;
@@ -106,127 +92,66 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, cons
                                                    : (base + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
   g_tc_last_pair = 0;
   if constexpr (H == 32 && MT == 1) {
-    if (!a.trace_states && tail.mode == 0 && pair_fits<Mode, STAB>(a.T, n_chunks, ctrls))
+    if (!a.trace_states && pair_fits<Mode, STAB>(a.T, n_chunks, ctrls))
       return go_pair<Mode, STAB>(a, frag, n_chunks, ctrls, stream);
   }
   // (MT = 2 serves K > 32768, whose grid never fits one wave: no on-chip eps')
   if constexpr (MT == 1) {
     if (store && !a.trace_states)
-      return go_store<H, MT, Mode, STAB, true>(a, frag, tail, n_chunks, ctrls, base + eps_bytes, stream);
+      return go_store<H, MT, Mode, STAB, true>(a, frag, n_chunks, ctrls, base + eps_bytes, stream);
   }
-  return go_store<H, MT, Mode, STAB, false>(a, frag, tail, n_chunks, ctrls, base, stream);
+  return go_store<H, MT, Mode, STAB, false>(a, frag, n_chunks, ctrls, base, stream);
 }
 template <int H, int Mode, bool STAB>
-cudaError_t by_mt(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail, int mt,
-                  int n_chunks, int ctrls, cudaStream_t stream) {
+cudaError_t by_mt(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int mt, int n_chunks, int ctrls,
+                  cudaStream_t stream) {
   if constexpr (H > 32) {  // one m16 tile per warp (register budget of the H = 64 accumulators)
-    return go<H, 1, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream);
+    return go<H, 1, Mode, STAB>(a, frag, n_chunks, ctrls, stream);
   } else {
-    return mt == 1 ? go<H, 1, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream)
-                   : go<H, 2, Mode, STAB>(a, frag, tail, n_chunks, ctrls, stream);
+    return mt == 1 ? go<H, 1, Mode, STAB>(a, frag, n_chunks, ctrls, stream)
+                   : go<H, 2, Mode, STAB>(a, frag, n_chunks, ctrls, stream);
   }
 }
 template <int H, int Mode>
-cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
-                    int mt, int n_chunks, int ctrls, cudaStream_t stream) {
+cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int mt, int n_chunks, int ctrls,
+                    cudaStream_t stream) {
   // the side-slip term (atan) is compiled in only when its weight is nonzero
-  return a.sys.cost.alpha_stab != 0.f ? by_mt<H, Mode, true>(a, frag, tail, mt, n_chunks, ctrls, stream)
-                                      : by_mt<H, Mode, false>(a, frag, tail, mt, n_chunks, ctrls, stream);
+  return a.sys.cost.alpha_stab != 0.f ? by_mt<H, Mode, true>(a, frag, mt, n_chunks, ctrls, stream)
+                                      : by_mt<H, Mode, false>(a, frag, mt, n_chunks, ctrls, stream);
 }
 }  // namespace tc_detail
 
 template <int H>
-cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
-                           mppi_dev::Acc* merged, unsigned* counters, const mppi_dev::TailArgs& ta, int ctrls,
-                           cudaStream_t stream) {
-  const size_t smem = ((std::max(mppi_dev::merge_smem_bytes(n), mppi_dev::fast_epilogue_smem_bytes<H>(ta.e.T)) + 15) &
-                       ~size_t(15)) +
-                      mppi_dev::tail_pre_bytes<H>(ta.e.T);
+cudaError_t launch_tail_tc(const mppi_dev::Acc* rows, int n, int stride, long long ctrl_stride, double lambda,
+                           const mppi_dev::TailArgs& ta, int ctrls, bool pdl, cudaStream_t stream) {
+  const size_t smem = mppi_dev::tail_smem_bytes<H>(n, ta.e.T);
   auto kern = mppi_dev::tail_kernel<H>;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  // programmatic dependent launch: the tail may launch before the previous
-  // kernel (K1 or the pre-merge) ends and waits for it on the device
+  // one CTA per controller; a programmatic dependent launch (pdl) of the group
+  // merge, so its prefetch of the plan, state and weights overlaps that kernel
   cudaLaunchConfig_t cfg = {};
-  // After a one-wave K1 (at most 2 CTAs of 4 chunks per SM) the tail's CTAs
-  // launch early (PDL) only where K1 left room: a quarter-size grid (4
-  // elements per CTA) is resident before K1 ends and merges as fast (c1:
-  // -5 us per iteration; profiles/README.md).  Multi-wave K1s keep one
-  // element per CTA.
-  static const int sms = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  int grid = std::min(stride, 296);
-  if (n <= 8 * sms) grid = (stride + 3) / 4;
-  if (const char* g = std::getenv("MPPI_TAIL_GRID")) grid = std::max(1, std::min(std::min(stride, 296), std::atoi(g)));
-  cfg.gridDim = dim3(grid, ctrls);
-  cfg.blockDim = dim3(mppi_dev::kMergeBlock);
+  cfg.gridDim = dim3(1, ctrls);
+  cfg.blockDim = dim3(mppi_dev::kTailBlock);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, partials, n, stride, ctrl_stride, lambda, merged, counters, ta);
-}
-
-template <int H>
-bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem) {
-  using tc_detail::kTcWarps;
-  // the tail works in the CTA's numerator buffers
-  const size_t red = sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
-  if (mppi_dev::merge_smem_bytes(n_chunks) > red || epilogue_smem > red) return false;
-  const size_t plan_bytes = (sizeof(float) * (2 * T + 2) + 15) & ~size_t(15);
-  const size_t eps_bytes = sizeof(float2) * kTcWarps * T * 16 * mt;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long ctas = (n_chunks + kTcWarps - 1) / kTcWarps;
-  // the launcher's own choice of the on-chip eps' variant (go() above)
-  const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
-                                                   : (plan_bytes + red + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
-  const size_t smem = plan_bytes + red + (store ? eps_bytes : 0);
-  int per_sm = 0;
-  auto occ = [&](auto kern) {
-    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kTcWarps, smem);
-    return r;
-  };
-  using mppi_dev::rollout_tc_kernel;
-  using mppi_dev::kPhilox;
-  cudaError_t e;
-  if constexpr (H > 32) {
-    e = store ? occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, true, false>)
-              : occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, false, false>);
-  } else {
-    if (mt == 1)
-      e = store ? occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, true, false>)
-                : occ(rollout_tc_kernel<H, 1, kTcWarps, kPhilox, false, false, false>);
-    else
-      e = store ? occ(rollout_tc_kernel<H, 2, kTcWarps, kPhilox, false, true, false>)
-                : occ(rollout_tc_kernel<H, 2, kTcWarps, kPhilox, false, false, false>);
-  }
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return ctas <= static_cast<long long>(per_sm) * sms;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, rows, n, stride, ctrl_stride, lambda, ta);
 }
 
 #ifdef TC_MODE
-template cudaError_t tc_detail::by_stab<TC_H, TC_MODE>(const mppi_dev::RolloutArgs<float>&, const uint32_t*,
-                                                        const mppi_dev::TailArgs&, int, int, int, cudaStream_t);
+template cudaError_t tc_detail::by_stab<TC_H, TC_MODE>(const mppi_dev::RolloutArgs<float>&, const uint32_t*, int,
+                                                        int, int, cudaStream_t);
 #endif
 #ifdef TC_TAIL
-template cudaError_t launch_tail_tc<TC_H>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*, unsigned*,
-                                          const mppi_dev::TailArgs&, int, cudaStream_t);
-template bool tc_coop_fits<TC_H>(int, int, int, size_t);
+template cudaError_t launch_tail_tc<TC_H>(const mppi_dev::Acc*, int, int, long long, double, const mppi_dev::TailArgs&,
+                                          int, bool, cudaStream_t);
 #endif
 
 }  // namespace mppi_host

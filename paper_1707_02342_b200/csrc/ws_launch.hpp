@@ -9,6 +9,7 @@
 #include "model.cuh"
 #include "rollout.cuh"
 #include "tail.cuh"
+#include "group.cuh"
 
 namespace mppi_host {
 
@@ -22,35 +23,29 @@ namespace tc_detail {
 extern int g_tc_last_pair;
 // the per-(H, noise mode) launchers, one translation unit each (tc_h*_*.cu)
 template <int H, int Mode>
-cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, const mppi_dev::TailArgs& tail,
-                    int mt, int n_chunks, int ctrls, cudaStream_t stream);
+cudaError_t by_stab(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int mt, int n_chunks, int ctrls,
+                    cudaStream_t stream);
 }  // namespace tc_detail
 
 // Tensor-core rollout (rollout_tc.cuh) for hidden width H (32, 64): `frag` is
 // the per-lane fragment table built by tc_build_fragments; n_chunks chunks of
 // 16*mt samples from a.chunk0 (mt is 1 at H = 64).
 template <int H>
-cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
-                              const mppi_dev::TailArgs& tail, int mode, int mt, int n_chunks, int ctrls,
-                              cudaStream_t stream);
-// The tensor-core tail in one launch: element-parallel merge, then the epilogue
-// by the last CTA (tail.cuh).  counters: one zero-initialised unsigned per controller.
+cudaError_t launch_rollout_tc(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int mode, int mt,
+                              int n_chunks, int ctrls, cudaStream_t stream);
+// The tensor-core tail: merge of the n group rows and the epilogue, one CTA
+// per controller (tail.cuh).
 template <int H>
-cudaError_t launch_tail_tc(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride, double lambda,
-                           mppi_dev::Acc* merged, unsigned* counters, const mppi_dev::TailArgs& ta, int ctrls,
-                           cudaStream_t stream);
-// Whether the cooperative tensor-core K1 (merge + epilogue inside, tail mode 1)
-// can run: the whole grid co-resident and the tail's scratch within the CTA's buffers.
-template <int H>
-bool tc_coop_fits(int T, int mt, int n_chunks, size_t epilogue_smem);
-extern template cudaError_t launch_tail_tc<32>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*,
-                                               unsigned*, const mppi_dev::TailArgs&, int, cudaStream_t);
-extern template cudaError_t launch_tail_tc<64>(const mppi_dev::Acc*, int, int, long long, double, mppi_dev::Acc*,
-                                               unsigned*, const mppi_dev::TailArgs&, int, cudaStream_t);
-extern template bool tc_coop_fits<32>(int, int, int, size_t);
-extern template bool tc_coop_fits<64>(int, int, int, size_t);
-// Element-parallel merge of n chunk partial rows into one row per controller (tail.cuh).
-cudaError_t launch_merge_elements(const mppi_dev::Acc* partials, int n, int stride, long long ctrl_stride,
-                                  double lambda, mppi_dev::Acc* merged, int ctrls, cudaStream_t stream);
+cudaError_t launch_tail_tc(const mppi_dev::Acc* rows, int n, int stride, long long ctrl_stride, double lambda,
+                           const mppi_dev::TailArgs& ta, int ctrls, bool pdl, cudaStream_t stream);
+extern template cudaError_t launch_tail_tc<32>(const mppi_dev::Acc*, int, int, long long, double,
+                                               const mppi_dev::TailArgs&, int, bool, cudaStream_t);
+extern template cudaError_t launch_tail_tc<64>(const mppi_dev::Acc*, int, int, long long, double,
+                                               const mppi_dev::TailArgs&, int, bool, cudaStream_t);
+// Fixed-group merge of the chunk partials (group.cuh): groups [g0, g0 + n_local)
+// of n_groups; programmatic dependent of the previous kernel when pdl.
+cudaError_t launch_group_merge(const mppi_dev::Acc* partials, long long partials_ctrl_stride, int n_chunks,
+                               int n_groups, int g0, int n_local, int stride, double lambda, mppi_dev::Acc* groups,
+                               long long groups_ctrl_stride, int ctrls, bool pdl, cudaStream_t stream);
 
 }  // namespace mppi_host

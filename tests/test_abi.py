@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol():
 def test_config_layout_and_defaults():
     lib = _lib.load()
     assert lib.mppi_gpu_config_sizeof() == ctypes.sizeof(_lib.ConfigC)
-    assert lib.mppi_gpu_abi_version() == 1
+    assert lib.mppi_gpu_abi_version() == 2
     cfg = _lib.ConfigC()
     lib.mppi_gpu_config_init(ctypes.byref(cfg))
     # SamplingParams{} (types.hpp:92-101), SGFilter{9,3}, CostParams{} (costs.hpp:46-54)

@@ -361,15 +361,15 @@ def test_kernel_variant_and_launch_count():
     g, _ = pair(w, "fp32", "philox")
     n0 = g.launch_count
     g.mpc_step(w.x0[0])
-    # the fp32 H = 32 vehicle path is the tensor-core K1 (+ the epilogue kernel)
+    # the fp32 H = 32 vehicle path is the tensor-core K1, the group merge and the tail
     assert "rollout_tc_pair_kernel" in g.kernel_variant  # one wave at this size: the warp-pair K1
-    assert g.launch_count - n0 in (1, 2)  # cooperative K1, or K1 + tail kernel (merge + epilogue)
+    assert g.launch_count - n0 == 3
     w64 = workload.make("c2", samples=256, horizon_steps=20)
     g64, _ = pair(w64, "fp32", "philox")
     n0 = g64.launch_count
     g64.mpc_step(w64.x0[0])
     assert "rollout_tc_kernel<f32,H=64" in g64.kernel_variant  # H = 64: tensor cores too (smem layer-2 weights)
-    assert g64.launch_count - n0 in (1, 2)
+    assert g64.launch_count - n0 == 3
 
 
 _TAIL_SCRIPT = r"""
@@ -382,33 +382,37 @@ w = workload.make('c1', samples=int(sys.argv[2]))
 g = Controller(w.params, w.bounds, w.sg, w.cost, hidden=32, precision='fp32', noise='philox')
 g.set_mlp(w.mlp); g.set_costmap(w.costmap)
 n0 = g.launch_count
+costs = g.rollout_batch(w.x0[0])
 u = [g.mpc_step(w.x0[0]).tolist() for _ in range(3)]
-print(json.dumps({'plan': g.plan.tolist(), 'u': u, 'launches': g.launch_count - n0, 'it': g.iteration}))
+print(json.dumps({'costs': costs.tolist(), 'plan': g.plan.tolist(), 'u': u, 'launches': g.launch_count - n0,
+                  'it': g.iteration, 'variant': g.kernel_variant}))
 """
 
 
-@pytest.mark.parametrize("K", [1920, 16384])
-def test_tail_styles_agree(K):
-    """The tensor-core path's two tails — the cooperative K1 (rollout, grid
-    barrier, element-parallel merge by all CTAs, grid barrier, epilogue by CTA
-    0: one launch per iteration) and K1 + merge kernel + epilogue kernel (the
-    shape used for large K and after the multi-rank all-gather) — run the same
-    arithmetic, so the plans are bit-identical."""
+def _run_script(script, args, env_over):
     import json
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for style in ("coop", "kernels"):  # MPPI_TAIL=coop opts in to the cooperative K1
-        env = dict(os.environ, MPPI_TAIL=style)
-        out = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, str(K)], env=env, capture_output=True,
-                             text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[style] = json.loads(out.stdout.strip().splitlines()[-1])
-    assert res["coop"]["launches"] == 3 and res["kernels"]["launches"] == 6
-    assert res["coop"]["plan"] == res["kernels"]["plan"] and res["coop"]["u"] == res["kernels"]["u"]
-    assert all(r["it"] == 3 for r in res.values())
+    env = dict(os.environ, **env_over)
+    out = subprocess.run([sys.executable, "-c", script, root] + [str(a) for a in args], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("K", [1920, 16384, 5000])
+def test_onchip_and_regenerated_eps_bit_identical(K):
+    """K1 keeps eps' on chip when its grid fits one wave and regenerates it
+    from the counters otherwise — a choice that depends on the rank's share of
+    the samples.  Both numerator passes (and the warp-pair kernel's) sum the
+    chunk rows in one order, so costs, plans and controls are bit-identical
+    (MPPI_TC_STORE=0 / 1 force the two; the pair kernel is off here)."""
+    res = {f: _run_script(_TAIL_SCRIPT, [K], {"MPPI_TC_STORE": f, "MPPI_TC_PAIR": "0"}) for f in ("0", "1")}
+    assert res["0"]["costs"] == res["1"]["costs"]
+    assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
+    assert all(r["it"] == 3 and r["launches"] == 10 for r in res.values())  # 1 + 3 x (K1, group merge, tail)
 
 
 _PAIR_SCRIPT = r"""
@@ -437,18 +441,7 @@ def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
     tensor-core kernel's operations: costs, plans and controls are
     bit-identical (odd T, a ragged last chunk, the side-slip cost term and the
     reference noise stream included)."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for flag in ("0", "1"):  # MPPI_TC_PAIR=0 / 1 force the single-warp / the pair kernel
-        env = dict(os.environ, MPPI_TC_PAIR=flag)
-        out = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(K), str(T), noise, form], env=env,
-                             capture_output=True, text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[flag] = json.loads(out.stdout.strip().splitlines()[-1])
+    res = {f: _run_script(_PAIR_SCRIPT, [K, T, noise, form], {"MPPI_TC_PAIR": f}) for f in ("0", "1")}
     assert "rollout_tc_pair_kernel" in res["1"]["variant"], res["1"]["variant"]
     assert "rollout_tc_kernel" in res["0"]["variant"], res["0"]["variant"]
     assert res["0"]["costs"] == res["1"]["costs"]
@@ -457,19 +450,7 @@ def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
 
 def test_tail_grid_does_not_change_results():
     """Each merged element is summed by one CTA in a fixed row order, so the
-    tail's grid size (one element per CTA, or the quarter-size grid used after
-    a one-wave K1) cannot change a bit of the plan."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for grid in ("296", "51", "7"):
-        env = dict(os.environ, MPPI_TAIL_GRID=grid)
-        out = subprocess.run([sys.executable, "-c", _TAIL_SCRIPT, root, "16384"], env=env, capture_output=True,
-                             text=True, timeout=300)
-        assert out.returncode == 0, out.stderr[-2000:]
-        res[grid] = json.loads(out.stdout.strip().splitlines()[-1])
+    tail's grid size cannot change a bit of the plan."""
+    res = {g: _run_script(_TAIL_SCRIPT, [16384], {"MPPI_TAIL_GRID": g}) for g in ("296", "51", "7")}
     assert res["296"]["plan"] == res["51"]["plan"] == res["7"]["plan"]
     assert res["296"]["u"] == res["51"]["u"] == res["7"]["u"]
