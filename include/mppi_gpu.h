@@ -179,6 +179,10 @@ int mppi_gpu_set_costmap_f32(mppi_gpu_handle* h, int controller, const float* va
  * clamp(shared + sigma * N(0,1)[seed, c, cell], -2.5, 2.5), generated on the
  * device from a counter stream. */
 int mppi_gpu_perturb_fleet_costmaps(mppi_gpu_handle* h, double sigma, uint64_t seed);
+/* Read back controller c's device costmap (width x height values as stored on
+ * the device: fp32 in the fp32 build, rounded to float here; the fleet's
+ * perturbed maps for parity checks). */
+int mppi_gpu_get_costmap_f32(mppi_gpu_handle* h, int controller, float* values_out);
 
 /* ---- ControllerState get/set (controller.hpp:40-58); also checkpoint/resume */
 int mppi_gpu_set_plan(mppi_gpu_handle* h, int controller, const double* U);

@@ -216,6 +216,13 @@ struct Mlp {
 template <class R>
 inline R mac(R acc, R w, R x) { return std::fma(w, x, acc); }
 
+// Evaluation-order variant of mlp_forward (accuracy studies only, default 0):
+// 1 sums every dot product over its inputs in DESCENDING order.  Two valid
+// fp32 evaluations of the same MLP differ by rounding alone; the spread of the
+// fp32 restatement between the two orders is the envelope an fp32 device
+// kernel with yet another order (tensor-core split products) is held to.
+inline int g_mlp_order = 0;
+
 // mlp_forward (dynamics.cpp:197-204): h1 = tanh(W1 in + b1),
 // h2 = tanh(W2 h1 + b2), out = W3 h2 + b3.  Accumulation starts from the bias
 // and runs over inputs in ascending order with fused multiply-adds (the
@@ -224,19 +231,29 @@ template <class R>
 void mlp_forward(const R in[6], const Mlp<R>& w, R out[4]) {
   const int H = w.H;
   R h1[64], h2[64];
+  const bool rev = g_mlp_order == 1;
   for (int j = 0; j < H; ++j) {
     R a = w.b1[j];
-    for (int i = 0; i < 6; ++i) a = mac(a, w.w1[j * 6 + i], in[i]);
+    for (int q = 0; q < 6; ++q) {
+      const int i = rev ? 5 - q : q;
+      a = mac(a, w.w1[j * 6 + i], in[i]);
+    }
     h1[j] = std::tanh(a);
   }
   for (int j = 0; j < H; ++j) {
     R a = w.b2[j];
-    for (int i = 0; i < H; ++i) a = mac(a, w.w2[j * H + i], h1[i]);
+    for (int q = 0; q < H; ++q) {
+      const int i = rev ? H - 1 - q : q;
+      a = mac(a, w.w2[j * H + i], h1[i]);
+    }
     h2[j] = std::tanh(a);
   }
   for (int o = 0; o < 4; ++o) {
     R a = w.b3[o];
-    for (int i = 0; i < H; ++i) a = mac(a, w.w3[o * H + i], h2[i]);
+    for (int q = 0; q < H; ++q) {
+      const int i = rev ? H - 1 - q : q;
+      a = mac(a, w.w3[o * H + i], h2[i]);
+    }
     out[o] = a;
   }
 }
@@ -839,6 +856,7 @@ using orc::AnyController;
 extern "C" {
 
 const char* oracle_last_error(void) { return orc::g_last_error.c_str(); }
+void oracle_set_mlp_order(int order) { orc::g_mlp_order = order; }
 
 uint64_t oracle_splitmix64(uint64_t x) { return orc::splitmix64(x); }
 uint64_t oracle_counter_hash(uint64_t seed, uint64_t stream, uint64_t it, uint64_t k, uint64_t t,

@@ -117,6 +117,7 @@ _SIGNATURES = {
     "mppi_gpu_set_costmap": (c_int, [c_void_p, c_int, _d, c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_set_costmap_f32": (c_int, [c_void_p, c_int, _P(c_float), c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_perturb_fleet_costmaps": (c_int, [c_void_p, c_double, c_uint64]),
+    "mppi_gpu_get_costmap_f32": (c_int, [c_void_p, c_int, _P(c_float)]),
     "mppi_gpu_set_plan": (c_int, [c_void_p, c_int, _d]),
     "mppi_gpu_get_plan": (c_int, [c_void_p, c_int, _d]),
     "mppi_gpu_set_iteration": (c_int, [c_void_p, c_int, c_uint64]),

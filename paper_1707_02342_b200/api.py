@@ -384,6 +384,12 @@ class Controller:
     def perturb_fleet_costmaps(self, sigma: float, seed: int) -> None:
         check(self._lib.mppi_gpu_perturb_fleet_costmaps(self._h, sigma, seed))
 
+    def get_costmap(self, like: "CostMap", controller: int = 0) -> "CostMap":
+        """Controller ``controller``'s device map (geometry of ``like``)."""
+        v = np.zeros(like.values.shape, dtype=np.float32)
+        check(self._lib.mppi_gpu_get_costmap_f32(self._h, controller, v.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+        return CostMap(v, like.x0, like.y0, like.resolution)
+
     # -- ControllerState ----------------------------------------------------
     def get_plan(self, controller: int = 0) -> np.ndarray:
         U = np.zeros((self.T, 2))

@@ -131,6 +131,12 @@ int mppi_gpu_set_costmap_f32(mppi_gpu_handle* h, int controller, const float* va
 int mppi_gpu_perturb_fleet_costmaps(mppi_gpu_handle* h, double sigma, uint64_t seed) {
   return with_handle(h, [&](auto& x) { x.perturb_fleet(sigma, seed); });
 }
+int mppi_gpu_get_costmap_f32(mppi_gpu_handle* h, int controller, float* values_out) {
+  return with_handle(h, [&](auto& x) {
+    if (!values_out) throw_invalid("get_costmap: null");
+    x.get_map_f32(controller, values_out);
+  });
+}
 int mppi_gpu_set_plan(mppi_gpu_handle* h, int controller, const double* U) {
   return with_handle(h, [&](auto& x) {
     if (!U) throw_invalid("set_plan: null");

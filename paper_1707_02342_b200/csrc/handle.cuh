@@ -187,7 +187,7 @@ struct Handle final : HandleBase {
   }
   std::string variant_name() const override {
     char buf[160];
-    if (use_tc && tc_detail::g_tc_last_pair)
+    if (use_tc && tc_pair_used == 1)
       std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);
     else if (use_tc)
@@ -221,6 +221,7 @@ struct Handle final : HandleBase {
   // tensor-core K1 (rollout_tc.cuh): fp32 vehicle model, H = 32; chunk = 16*tc_mt
   bool use_tc = false;
   int tc_mt = 2;
+  int tc_pair_used = -1;  // whether this handle's last K1 launch was the warp-pair kernel (-1: none yet)
   DevBuf<uint32_t> d_tcfrag;
   // tensor-core tail (tail.cuh): merge of the group rows + epilogue, one CTA per controller
   DevBuf<unsigned char> d_plantw;  // MlpParams<float, H> (the plant step of the tail)
@@ -587,6 +588,17 @@ struct Handle final : HandleBase {
     invalidate_graphs();
   }
 
+  void get_map_f32(int ctrl, float* out) override {
+    check_ctrl(ctrl);
+    if (!has_map) throw_invalid("get_costmap: no costmap set");
+    std::vector<const R*> ptrs(C);
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaMemcpy(ptrs.data(), d_map_ptrs.p, C * sizeof(const R*), cudaMemcpyDeviceToHost));
+    const size_t n = static_cast<size_t>(map_w) * map_h;
+    std::vector<R> v(n);
+    CUDA_TRY(cudaMemcpy(v.data(), ptrs[ctrl], n * sizeof(R), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) out[i] = static_cast<float>(v[i]);
+  }
   void set_plan(int ctrl, const double* U) {
     check_ctrl(ctrl);
     std::vector<R> v(2 * T);
@@ -765,6 +777,7 @@ struct Handle final : HandleBase {
       if constexpr (std::is_same<R, float>::value)
         CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, mode, tc_mt,
                                                                           chunk_hi - chunk_lo, C, stream));
+      tc_pair_used = tc_detail::g_tc_last_pair;
     } else if (use_ws) {
       launch_ws(a, mode, grid);
     } else {

@@ -22,6 +22,7 @@ struct HandleBase {
   virtual void set_map_f64(int ctrl, const double* v, int w, int h, double x0, double y0, double res) = 0;
   virtual void set_map_f32(int ctrl, const float* v, int w, int h, double x0, double y0, double res) = 0;
   virtual void perturb_fleet(double sigma, uint64_t seed) = 0;
+  virtual void get_map_f32(int ctrl, float* out) = 0;
   virtual void set_plan(int ctrl, const double* U) = 0;
   virtual void get_plan(int ctrl, double* U) = 0;
   virtual void set_iteration(int ctrl, uint64_t it) = 0;

@@ -23,6 +23,7 @@ _d = POINTER(c_double)
 
 _SIG = {
     "oracle_last_error": (c_char_p, []),
+    "oracle_set_mlp_order": (None, [c_int]),
     "oracle_splitmix64": (c_uint64, [c_uint64]),
     "oracle_counter_hash": (c_uint64, [c_uint64] * 6),
     "oracle_counter_normal": (c_double, [c_uint64] * 5 + [c_int]),
