@@ -57,7 +57,8 @@ enum {
   MPPI_ERR_RUNTIME = 3,
   MPPI_ERR_CUDA = 4,
   MPPI_ERR_NCCL = 5,
-  MPPI_ERR_UNSUPPORTED = 6
+  MPPI_ERR_UNSUPPORTED = 6,
+  MPPI_ERR_DOMAIN = 7          /* std::domain_error: brush_tire_force outside the friction circle, dynamics.cpp:25-27 */
 };
 
 /* Perturbation source.  INJECTED reads a caller-provided batch in the
@@ -78,7 +79,29 @@ enum { MPPI_FP32 = 0, MPPI_FP64 = 1 };
  * (dynamics.hpp:151-162): the 25 basis functions of eval_basis
  * (dynamics.cpp:83-133) times the 25 x 4 Theta (step_basis_model,
  * dynamics.cpp:152-157), with the same costs as VEHICLE_MLP. */
-enum { MPPI_SYSTEM_VEHICLE_MLP = 0, MPPI_SYSTEM_QUADRATIC = 1, MPPI_SYSTEM_VEHICLE_BASIS = 2 };
+enum {
+  MPPI_SYSTEM_VEHICLE_MLP = 0,
+  MPPI_SYSTEM_QUADRATIC = 1,
+  MPPI_SYSTEM_VEHICLE_BASIS = 2,
+  /* make_vehicle_system over BicycleTruthModel (dynamics.hpp:176-183): the
+   * kinematic-dynamic bicycle with brush tires (step_bicycle_truth,
+   * dynamics.cpp:51-81) as the controller's own model. */
+  MPPI_SYSTEM_VEHICLE_BICYCLE = 3
+};
+
+/* BicycleParams (dynamics.hpp:42-62); mppi_bicycle_params_init fills the
+ * reference defaults. */
+typedef struct mppi_bicycle_params {
+  double mass;
+  double yaw_inertia;
+  double a;
+  double b;
+  double stiffness;
+  double mu;
+  double load;
+  double steer_scale;
+  double force_scale;
+} mppi_bicycle_params;
 
 /* Weight rule (controller.hpp:32): information-theoretic softmin or CEM
  * elite averaging (weights.cpp:8-53), both on the device. */
@@ -175,6 +198,12 @@ int mppi_gpu_set_costmap(mppi_gpu_handle* h, int controller, const double* value
 int mppi_gpu_set_costmap_f32(mppi_gpu_handle* h, int controller, const float* values,
                              int width, int height, double x0, double y0,
                              double resolution);
+/* BicycleTruthModel parameters of a MPPI_SYSTEM_VEHICLE_BICYCLE handle
+ * (BicycleParams::validate: every entry finite and > 0).  The rollout clamps
+ * the throttle to the control bounds, so the reference's friction-circle
+ * domain_error is checked once here: force_scale * max |throttle bound| must
+ * not exceed mu * load (MPPI_ERR_DOMAIN otherwise). */
+int mppi_gpu_set_dynamics_bicycle(mppi_gpu_handle* h, const mppi_bicycle_params* p);
 /* Fleet maps (BASELINE config 3): controller c gets
  * clamp(shared + sigma * N(0,1)[seed, c, cell], -2.5, 2.5), generated on the
  * device from a counter stream. */
@@ -306,6 +335,59 @@ int mppi_gpu_fp32_peak_probe(int device, double* tflops_out, double* sm_clock_mh
  * m16n8k16 f16 -> f32 throughput (TFLOP/s) and MUFU ex2 throughput (G lane
  * operations/s), the best of a few full-chip probe launches. */
 int mppi_gpu_pipe_peak_probe(int device, double* hmma_tflops_out, double* mufu_gops_out);
+
+/* ---- closed-loop driver: simulate_episode (simulator.cpp:102-177) ----------- */
+/* Additive velocity / yaw-rate kick applied to the plant after the step that
+ * ends at time_s (Disturbance, simulator.hpp:10-16). */
+typedef struct mppi_disturbance {
+  double time_s;
+  double dv_x;
+  double dv_y;
+  double dtheta_dot;
+} mppi_disturbance;
+/* SimConfig (simulator.hpp:72-88) minus the parts the handle already holds
+ * (sampling, weight rule, SG filter, bounds, costs, terminal cost). */
+typedef struct mppi_sim_config {
+  double episode_s;                  /* steps = lround(episode_s / dt) */
+  int32_t exec_noise;                /* execution noise on the applied input */
+  int32_t has_exec_noise_diag;       /* 0: the sampling variances */
+  double exec_noise_diag[2];         /* variances */
+  int32_t has_estimate_noise;        /* 0: exact state feedback */
+  double estimate_noise_std[7];      /* standard deviations per state entry */
+  mppi_bicycle_params plant;         /* the truth plant */
+  double start_state[7];
+  int32_t n_disturbances;
+  const mppi_disturbance* disturbances;
+} mppi_sim_config;
+/* StepRecord (simulator.hpp:17-24): the plant state when the control was
+ * computed, the clamped command, the realised input (command + execution
+ * noise, before the plant's clamp), state_cost(x, 0) and h at the position. */
+typedef struct mppi_sim_record {
+  double time;
+  double state[7];
+  double commanded[2];
+  double realized[2];
+  double cost;
+  double map_h;
+} mppi_sim_record;
+/* Reference defaults: SimConfig{} with BicycleParams{} and exec_noise on. */
+void mppi_sim_config_init(mppi_sim_config* cfg);
+/* One closed-loop episode on a single-controller handle: per step the state
+ * estimate (+ estimate noise, counter stream kStreamEstimateNoise), mpc_step
+ * on the device, execution noise (kStreamExecutionNoise), the clamped bicycle
+ * truth step on the host, disturbances.  Deterministic given the handle's
+ * seed.  records_out holds `capacity` records; *n_steps_out is the number
+ * written; *aborted_out is 1 if a non-finite state ended the episode early.
+ * The handle's controller-0 costmap is read back for the recorded cost. */
+int mppi_sim_episode(mppi_gpu_handle* h, const mppi_sim_config* cfg, mppi_sim_record* records_out,
+                     int capacity, int* n_steps_out, int* aborted_out);
+/* Host evaluations of the truth model (reference pins; no device):
+ * brush_tire_force (dynamics.cpp:23-43) and step_bicycle_truth
+ * (dynamics.cpp:51-81, no clamp: the input is the applied one). */
+void mppi_bicycle_params_init(mppi_bicycle_params* p);
+int mppi_brush_tire_force(double alpha, double u_F, const mppi_bicycle_params* p, double* force_out);
+int mppi_bicycle_step(const mppi_bicycle_params* p, const double x[7], const double v[2], double dt,
+                      double x_next_out[7]);
 
 /* ---- host-side workload generation (no GPU needed) ------------------------- */
 /* Xavier-uniform MLP weights from a seed (BASELINE configs): U(-a, a),

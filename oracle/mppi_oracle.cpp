@@ -452,6 +452,80 @@ System<R> make_basis_system(const std::vector<R>& theta, const R lo[2], const R 
   return s;
 }
 
+// ------------------------------------------------ bicycle truth model -------
+// BicycleParams (dynamics.hpp:42-62), entries in declaration order.
+template <class R>
+struct Bicycle {
+  R mass = R(22.0), yaw_inertia = R(1.8), a = R(0.45), b = R(0.35), stiffness = R(180.0), mu = R(0.65),
+    load = R(107.9), steer_scale = R(0.35), force_scale = R(35.0);
+};
+
+// brush_tire_force (dynamics.cpp:23-43)
+template <class R>
+R brush_tire_force(R alpha, R u_F, const Bicycle<R>& p) {
+  const R limit = p.mu * p.load;
+  if (std::abs(u_F) > limit)
+    throw std::domain_error("brush_tire_force: |u_F| exceeds the friction circle mu*F_z");
+  const R xi = std::sqrt(limit * limit - u_F * u_F) / limit;
+  if (xi == R(0)) return R(0);
+  const R sign = (alpha >= R(0)) ? R(1) : R(-1);
+  const R crossover = std::atan(R(3) * xi * p.mu * p.load / p.stiffness);
+  if (std::abs(alpha) >= crossover) return -p.mu * xi * p.load * sign;
+  const R ta = std::tan(alpha);
+  const R c = p.stiffness;
+  return -c * ta + c * c / (R(3) * xi * p.mu * p.load) * ta * std::abs(ta) -
+         c * c * c / (R(27) * p.mu * p.mu * xi * xi * p.load * p.load) * ta * ta * ta;
+}
+
+// step_bicycle_truth (dynamics.cpp:51-81), kSlipGuardSpeed = 0.1; roll unchanged
+template <class R>
+void step_bicycle(const R x[7], const R v[2], R dt, const Bicycle<R>& p, R n[7]) {
+  if (!(dt > R(0))) throw std::invalid_argument("step_bicycle_truth: dt must be > 0");
+  const R u_delta = p.steer_scale * v[0];
+  const R u_F = p.force_scale * v[1];
+  const R r = x[6];
+  R alpha_f, alpha_r;
+  if (x[4] > R(0.1)) {
+    const R beta = x[5] / x[4];
+    alpha_f = std::atan(beta + p.a * r / x[4]) - u_delta;
+    alpha_r = std::atan(beta - p.b * r / x[4]);
+  } else {
+    alpha_f = -u_delta;
+    alpha_r = R(0);
+  }
+  const R f_yf = brush_tire_force<R>(alpha_f, u_F, p);
+  const R f_yr = brush_tire_force<R>(alpha_r, u_F, p);
+  for (int i = 0; i < 7; ++i) n[i] = x[i];
+  n[0] += (std::cos(x[2]) * x[4] - std::sin(x[2]) * x[5]) * dt;
+  n[1] += (std::sin(x[2]) * x[4] + std::cos(x[2]) * x[5]) * dt;
+  n[2] += r * dt;
+  n[4] += ((u_F - f_yf * std::sin(u_delta)) / p.mass + r * x[5]) * dt;
+  n[5] += ((f_yf + f_yr) / p.mass - r * x[4]) * dt;
+  n[6] += ((p.a * f_yf - p.b * f_yr) / p.yaw_inertia) * dt;
+}
+
+// make_vehicle_system (controller.cpp:7-35) over a BicycleTruthModel
+// (dynamics.hpp:176-183): clamp, then step_bicycle_truth.
+template <class R>
+System<R> make_bicycle_system(const Bicycle<R>& bike, const R lo[2], const R hi[2], const Map<R>& map,
+                              const Cost<R>& cp, R dt, int horizon, bool with_terminal) {
+  System<R> s;
+  s.state_dim = 7;
+  s.control_dim = 2;
+  const R l0 = lo[0], l1 = lo[1], h0 = hi[0], h1 = hi[1];
+  s.step = [&bike, l0, l1, h0, h1, dt](const R* x, const R* v, int, R* xn) {
+    const R g[2] = {clampv(v[0], l0, h0), clampv(v[1], l1, h1)};
+    step_bicycle<R>(x, g, dt, bike, xn);
+  };
+  s.running_cost = [&map, &cp](const R* x, int t) { return state_cost(x, t, map, cp); };
+  if (with_terminal) {
+    s.terminal_cost = [&map, &cp, horizon](const R* x) { return state_cost(x, horizon, map, cp); };
+  } else {
+    s.terminal_cost = [](const R*) { return R(0); };
+  }
+  return s;
+}
+
 // quadratic_system (test_controller.cpp:23-37), running cost scaled.
 template <class R>
 System<R> make_quadratic_system(int m, R dt, R cost_scale) {
@@ -635,6 +709,7 @@ struct Controller {
   std::vector<R> injected;   // reference layout, INJECTED mode
   Batch<R> last_batch;       // batch of the last rollout (post-mutation)
   std::vector<R> theta;  // basis-function model coeffs, theta[b*4 + o]
+  Bicycle<R> bike;       // bicycle truth model parameters
   bool has_mlp = false, has_map = false;
 
   int T() const { return p.horizon_steps; }
@@ -647,6 +722,9 @@ struct Controller {
     if (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS)
       return make_basis_system<R>(theta, lo, hi, map, cost, static_cast<R>(p.dt), p.horizon_steps,
                                   cfg.with_terminal != 0);
+    if (cfg.system == MPPI_SYSTEM_VEHICLE_BICYCLE)
+      return make_bicycle_system<R>(bike, lo, hi, map, cost, static_cast<R>(p.dt), p.horizon_steps,
+                                    cfg.with_terminal != 0);
     return make_vehicle_system<R>(mlp, lo, hi, map, cost, static_cast<R>(p.dt), p.horizon_steps,
                                   cfg.with_terminal != 0);
   }
@@ -830,6 +908,9 @@ int guard(F&& f) {
   } catch (const std::invalid_argument& e) {
     g_last_error = e.what();
     return MPPI_ERR_INVALID_ARGUMENT;
+  } catch (const std::domain_error& e) {
+    g_last_error = e.what();
+    return MPPI_ERR_DOMAIN;
   } catch (const std::exception& e) {
     g_last_error = e.what();
     return MPPI_ERR_RUNTIME;
@@ -1031,6 +1112,32 @@ int oracle_set_theta(AnyController* h, const double* theta) {
     }
     c.has_mlp = true;
   });
+}
+int oracle_set_bicycle(AnyController* h, const double p[9]) {
+  return orc::dispatch(h, [&](auto& c) {
+    using R = typename std::decay_t<decltype(c.plan)>::value_type;
+    for (int i = 0; i < 9; ++i)
+      if (!(p[i] > 0.0) || !std::isfinite(p[i])) throw std::invalid_argument("BicycleParams: all parameters must be positive");
+    c.bike = orc::Bicycle<R>{static_cast<R>(p[0]), static_cast<R>(p[1]), static_cast<R>(p[2]), static_cast<R>(p[3]),
+                             static_cast<R>(p[4]), static_cast<R>(p[5]), static_cast<R>(p[6]), static_cast<R>(p[7]),
+                             static_cast<R>(p[8])};
+    c.has_mlp = true;
+  });
+}
+// brush_tire_force / step_bicycle_truth in double (the reference pins); 4 = domain_error
+int oracle_brush_tire_force(double alpha, double u_F, const double p[9], double* out) {
+  const orc::Bicycle<double> b{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8]};
+  try {
+    *out = orc::brush_tire_force<double>(alpha, u_F, b);
+  } catch (const std::domain_error& e) {
+    orc::g_last_error = e.what();
+    return MPPI_ERR_DOMAIN;
+  }
+  return 0;
+}
+int oracle_step_bicycle(const double x[7], const double v[2], double dt, const double p[9], double out[7]) {
+  const orc::Bicycle<double> b{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8]};
+  return orc::guard([&] { orc::step_bicycle<double>(x, v, dt, b, out); });
 }
 // eval_basis (dynamics.cpp:83-133) in double: x_d = (roll, v_x, v_y, r), v = (steer, throttle).
 int oracle_eval_basis(const double x_d[4], const double v[2], double phi[25]) {

@@ -22,10 +22,11 @@ MPPI_ERR_RUNTIME = 3
 MPPI_ERR_CUDA = 4
 MPPI_ERR_NCCL = 5
 MPPI_ERR_UNSUPPORTED = 6
+MPPI_ERR_DOMAIN = 7
 
 NOISE_INJECTED, NOISE_REF_SPLITMIX, NOISE_PHILOX = 0, 1, 2
 FP32, FP64 = 0, 1
-SYSTEM_VEHICLE_MLP, SYSTEM_QUADRATIC, SYSTEM_VEHICLE_BASIS = 0, 1, 2
+SYSTEM_VEHICLE_MLP, SYSTEM_QUADRATIC, SYSTEM_VEHICLE_BASIS, SYSTEM_VEHICLE_BICYCLE = 0, 1, 2, 3
 WEIGHT_IT, WEIGHT_CEM = 0, 1
 
 
@@ -57,6 +58,10 @@ class MppiRuntimeError(MppiError, RuntimeError):
     """std::runtime_error in the reference."""
 
 
+class DomainError(MppiError, ArithmeticError):
+    """std::domain_error in the reference (brush_tire_force, dynamics.cpp:25-27)."""
+
+
 _ERRORS = {
     MPPI_ERR_INVALID_ARGUMENT: InvalidArgument,
     MPPI_ERR_NONFINITE: NonFiniteCost,
@@ -64,6 +69,7 @@ _ERRORS = {
     MPPI_ERR_CUDA: DeviceError,
     MPPI_ERR_NCCL: DeviceError,
     MPPI_ERR_UNSUPPORTED: Unsupported,
+    MPPI_ERR_DOMAIN: DomainError,
 }
 
 
@@ -102,6 +108,35 @@ class ConfigC(ctypes.Structure):
     ]
 
 
+class BicycleParamsC(ctypes.Structure):
+    _fields_ = [(n, c_double) for n in (
+        "mass", "yaw_inertia", "a", "b", "stiffness", "mu", "load", "steer_scale", "force_scale")]
+
+
+class DisturbanceC(ctypes.Structure):
+    _fields_ = [("time_s", c_double), ("dv_x", c_double), ("dv_y", c_double), ("dtheta_dot", c_double)]
+
+
+class SimConfigC(ctypes.Structure):
+    _fields_ = [
+        ("episode_s", c_double),
+        ("exec_noise", c_int32),
+        ("has_exec_noise_diag", c_int32),
+        ("exec_noise_diag", c_double * 2),
+        ("has_estimate_noise", c_int32),
+        ("estimate_noise_std", c_double * 7),
+        ("plant", BicycleParamsC),
+        ("start_state", c_double * 7),
+        ("n_disturbances", c_int32),
+        ("disturbances", POINTER(DisturbanceC)),
+    ]
+
+
+class SimRecordC(ctypes.Structure):
+    _fields_ = [("time", c_double), ("state", c_double * 7), ("commanded", c_double * 2),
+                ("realized", c_double * 2), ("cost", c_double), ("map_h", c_double)]
+
+
 _P = POINTER
 _d = _P(c_double)
 _SIGNATURES = {
@@ -114,6 +149,12 @@ _SIGNATURES = {
     "mppi_gpu_destroy": (c_int, [c_void_p]),
     "mppi_gpu_set_dynamics_mlp": (c_int, [c_void_p, c_int, _d, _d, _d, _d, _d, _d]),
     "mppi_gpu_set_dynamics_basis": (c_int, [c_void_p, _d]),
+    "mppi_gpu_set_dynamics_bicycle": (c_int, [c_void_p, _P(BicycleParamsC)]),
+    "mppi_bicycle_params_init": (None, [_P(BicycleParamsC)]),
+    "mppi_brush_tire_force": (c_int, [c_double, c_double, _P(BicycleParamsC), _d]),
+    "mppi_bicycle_step": (c_int, [_P(BicycleParamsC), _d, _d, c_double, _d]),
+    "mppi_sim_config_init": (None, [_P(SimConfigC)]),
+    "mppi_sim_episode": (c_int, [c_void_p, _P(SimConfigC), _P(SimRecordC), c_int, _P(c_int), _P(c_int)]),
     "mppi_gpu_set_costmap": (c_int, [c_void_p, c_int, _d, c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_set_costmap_f32": (c_int, [c_void_p, c_int, _P(c_float), c_int, c_int, c_double, c_double, c_double]),
     "mppi_gpu_perturb_fleet_costmaps": (c_int, [c_void_p, c_double, c_uint64]),

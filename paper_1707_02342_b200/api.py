@@ -33,7 +33,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import (DeviceError, InvalidArgument, MppiError, NonFiniteCost, Unsupported, check, dptr)
+from ._lib import (DeviceError, DomainError, InvalidArgument, MppiError, NonFiniteCost, Unsupported, check, dptr)
 
 __all__ = [
     "SamplingParams", "ControlBounds", "CostParams", "SGFilter", "WeightResult", "MlpWeights",
@@ -236,6 +236,124 @@ def sg_coefficients(window: int, degree: int) -> np.ndarray:
     return out
 
 
+@dataclass
+class BicycleParams:
+    """BicycleParams (dynamics.hpp:42-62): the truth plant and the
+    "vehicle_bicycle" rollout system."""
+    mass: float = 22.0
+    yaw_inertia: float = 1.8
+    a: float = 0.45
+    b: float = 0.35
+    stiffness: float = 180.0
+    mu: float = 0.65
+    load: float = 107.9
+    steer_scale: float = 0.35
+    force_scale: float = 35.0
+
+    def c(self) -> "_lib.BicycleParamsC":
+        return _lib.BicycleParamsC(*[float(getattr(self, f)) for f in BicycleParams.__dataclass_fields__])
+
+
+def brush_tire_force(alpha: float, u_F: float, p: BicycleParams = BicycleParams()) -> float:
+    """brush_tire_force (dynamics.cpp:23-43) on the host (DomainError outside the friction circle)."""
+    out = ctypes.c_double()
+    pc = p.c()
+    check(_lib.load().mppi_brush_tire_force(alpha, u_F, ctypes.byref(pc), ctypes.byref(out)))
+    return out.value
+
+
+def step_bicycle_truth(x, v, dt: float, p: BicycleParams = BicycleParams()) -> np.ndarray:
+    """step_bicycle_truth (dynamics.cpp:51-81) on the host; v is the applied input."""
+    xa = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(7))
+    va = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(2))
+    out = np.zeros(7)
+    pc = p.c()
+    check(_lib.load().mppi_bicycle_step(ctypes.byref(pc), dptr(xa), dptr(va), dt, dptr(out)))
+    return out
+
+
+@dataclass
+class Disturbance:
+    """Disturbance (simulator.hpp:10-16)."""
+    time_s: float = 0.0
+    dv_x: float = 0.0
+    dv_y: float = 0.0
+    dtheta_dot: float = 0.0
+
+
+@dataclass
+class SimConfig:
+    """The closed-loop parts of SimConfig (simulator.hpp:72-88); sampling,
+    bounds, costs, SG and the weight rule live in the controller."""
+    episode_s: float = 30.0
+    exec_noise: bool = True
+    exec_noise_diag: Optional[Sequence[float]] = None    # variances; None = sampling covariance
+    estimate_noise_std: Optional[Sequence[float]] = None  # 7 std devs; None = exact state feedback
+    plant: BicycleParams = field(default_factory=BicycleParams)
+    start_state: Sequence[float] = (0.0,) * 7
+    disturbances: Sequence[Disturbance] = ()
+
+
+@dataclass
+class EpisodeTrace:
+    """EpisodeTrace (simulator.hpp:26-32) as arrays, one row per step."""
+    time: np.ndarray
+    state: np.ndarray       # n x 7
+    commanded: np.ndarray   # n x 2
+    realized: np.ndarray    # n x 2
+    cost: np.ndarray
+    map_h: np.ndarray
+    dt: float
+    seed: int
+    aborted: bool
+
+
+TRACE_HEADER = ("time_s,p_x,p_y,theta,roll,v_x,v_y,theta_dot,steer_cmd,throttle_cmd,"
+                "steer_real,throttle_real,cost,map_h")
+
+
+def save_trace(trace: EpisodeTrace, path: str) -> None:
+    """save_trace (simulator.cpp:180-200): the documented columns, %.17g."""
+    with open(path, "w") as f:
+        f.write(TRACE_HEADER + "\n")
+        for i in range(len(trace.time)):
+            row = [trace.time[i], *trace.state[i], *trace.commanded[i], *trace.realized[i], trace.cost[i],
+                   trace.map_h[i]]
+            f.write(",".join("%.17g" % float(v) for v in row) + "\n")
+
+
+def simulate_episode(ctrl: "Controller", sim: SimConfig) -> EpisodeTrace:
+    """simulate_episode (simulator.cpp:102-177) over a single-controller handle:
+    mpc_step on the device every period, the bicycle truth plant on the host."""
+    c = _lib.SimConfigC()
+    _lib.load().mppi_sim_config_init(ctypes.byref(c))
+    c.episode_s = sim.episode_s
+    c.exec_noise = int(bool(sim.exec_noise))
+    if sim.exec_noise_diag is not None:
+        c.has_exec_noise_diag = 1
+        c.exec_noise_diag[0], c.exec_noise_diag[1] = (float(v) for v in sim.exec_noise_diag)
+    if sim.estimate_noise_std is not None:
+        if len(sim.estimate_noise_std) != 7:
+            raise InvalidArgument(_lib.MPPI_ERR_INVALID_ARGUMENT, "estimate_noise_std needs 7 entries")
+        c.has_estimate_noise = 1
+        for i, v in enumerate(sim.estimate_noise_std):
+            c.estimate_noise_std[i] = float(v)
+    c.plant = sim.plant.c()
+    for i, v in enumerate(sim.start_state):
+        c.start_state[i] = float(v)
+    dist = (_lib.DisturbanceC * max(1, len(sim.disturbances)))(
+        *[_lib.DisturbanceC(d.time_s, d.dv_x, d.dv_y, d.dtheta_dot) for d in sim.disturbances])
+    c.n_disturbances = len(sim.disturbances)
+    c.disturbances = ctypes.cast(dist, ctypes.POINTER(_lib.DisturbanceC))
+    steps = int(round(sim.episode_s / ctrl.params.dt)) + 1
+    recs = (_lib.SimRecordC * steps)()
+    n, ab = ctypes.c_int(), ctypes.c_int()
+    check(_lib.load().mppi_sim_episode(ctrl._h, ctypes.byref(c), recs, steps, ctypes.byref(n), ctypes.byref(ab)))
+    arr = np.ctypeslib.as_array(ctypes.cast(recs, ctypes.POINTER(ctypes.c_double)), shape=(steps, 14))[:n.value]
+    return EpisodeTrace(arr[:, 0].copy(), arr[:, 1:8].copy(), arr[:, 8:10].copy(), arr[:, 10:12].copy(),
+                        arr[:, 12].copy(), arr[:, 13].copy(), ctrl.params.dt, int(ctrl.params.seed), bool(ab.value))
+
+
 def device_count() -> int:
     return int(_lib.load().mppi_gpu_device_count())
 
@@ -257,6 +375,7 @@ def fp32_peak_tflops(device: int = 0):
 _NOISE = {"injected": _lib.NOISE_INJECTED, "ref_splitmix": _lib.NOISE_REF_SPLITMIX, "philox": _lib.NOISE_PHILOX}
 _PREC = {"fp32": _lib.FP32, "fp64": _lib.FP64}
 _SYSTEM = {"vehicle_mlp": _lib.SYSTEM_VEHICLE_MLP, "quadratic": _lib.SYSTEM_QUADRATIC,
+           "vehicle_bicycle": _lib.SYSTEM_VEHICLE_BICYCLE,
            "vehicle_basis": _lib.SYSTEM_VEHICLE_BASIS}
 
 
@@ -364,6 +483,11 @@ class Controller:
     def set_mlp(self, w: MlpWeights) -> None:
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (w.w1, w.b1, w.w2, w.b2, w.w3, w.b3)]
         check(self._lib.mppi_gpu_set_dynamics_mlp(self._h, w.hidden, *[dptr(a) for a in arrs]))
+
+    def set_bicycle(self, p: BicycleParams = BicycleParams()) -> None:
+        """BicycleTruthModel as the controller's model ("vehicle_bicycle" system)."""
+        pc = p.c()
+        check(self._lib.mppi_gpu_set_dynamics_bicycle(self._h, ctypes.byref(pc)))
 
     def set_basis(self, theta) -> None:
         """BasisFunctionModel Theta (dynamics.hpp:75-82): 25 x 4, coeffs(b, o)."""

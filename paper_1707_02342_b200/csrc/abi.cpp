@@ -114,6 +114,12 @@ int mppi_gpu_set_dynamics_basis(mppi_gpu_handle* h, const double* theta) {
     x.set_basis(theta);
   });
 }
+int mppi_gpu_set_dynamics_bicycle(mppi_gpu_handle* h, const mppi_bicycle_params* p) {
+  return with_handle(h, [&](auto& x) {
+    if (!p) throw_invalid("set_dynamics_bicycle: null params");
+    x.set_bicycle(*p);
+  });
+}
 int mppi_gpu_set_costmap(mppi_gpu_handle* h, int controller, const double* values, int width,
                          int height, double x0, double y0, double resolution) {
   return with_handle(h, [&](auto& x) {

@@ -32,6 +32,8 @@ __device__ __forceinline__ float tanh_r(float x) { return tanhf(x); }
 __device__ __forceinline__ double tanh_r(double x) { return tanh(x); }
 __device__ __forceinline__ float exp_r(float x) { return expf(x); }
 __device__ __forceinline__ double exp_r(double x) { return exp(x); }
+__device__ __forceinline__ float sqrt_r(float x) { return __fsqrt_rn(x); }
+__device__ __forceinline__ double sqrt_r(double x) { return __dsqrt_rn(x); }
 __device__ __forceinline__ float atan_r(float x) { return atanf(x); }
 __device__ __forceinline__ double atan_r(double x) { return atan(x); }
 __device__ __forceinline__ float tan_r(float x) { return tanf(x); }

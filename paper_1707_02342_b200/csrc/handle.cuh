@@ -200,7 +200,9 @@ struct Handle final : HandleBase {
       std::snprintf(buf, sizeof(buf), "rollout_kernel<%s,H=%d,%s,noise=%d,block=%d>",
                     std::is_same<R, double>::value ? "f64" : "f32", H,
                     cfg.system == MPPI_SYSTEM_QUADRATIC ? "quadratic"
-                    : (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS ? "vehicle_basis" : "vehicle_mlp"),
+                    : (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS     ? "vehicle_basis"
+                       : cfg.system == MPPI_SYSTEM_VEHICLE_BICYCLE ? "vehicle_bicycle"
+                                                                   : "vehicle_mlp"),
                     cfg.noise_mode, kBlock);
     return buf;
   }
@@ -243,6 +245,7 @@ struct Handle final : HandleBase {
   // weights (host copies; by-value kernel parameters) + device copy for the
   // by-pointer variant
   ThetaDev<R> theta_r{};  // VEHICLE_BASIS coefficients
+  BicycleDev<R> bike_r{};  // VEHICLE_BICYCLE parameters
   std::unique_ptr<MlpParams<R, 32>> w32;
   std::unique_ptr<MlpParams<R, 64>> w64;
   DevBuf<MlpParams<R, 64>> d_w64;
@@ -440,7 +443,7 @@ struct Handle final : HandleBase {
     if (c.noise_mode < 0 || c.noise_mode > 2) throw_invalid("noise_mode");
     if (c.precision != MPPI_FP32 && c.precision != MPPI_FP64) throw_invalid("precision");
     if (c.system != MPPI_SYSTEM_VEHICLE_MLP && c.system != MPPI_SYSTEM_QUADRATIC &&
-        c.system != MPPI_SYSTEM_VEHICLE_BASIS)
+        c.system != MPPI_SYSTEM_VEHICLE_BASIS && c.system != MPPI_SYSTEM_VEHICLE_BICYCLE)
       throw_invalid("system");
     if (c.mlp_hidden != 32 && c.mlp_hidden != 64) throw_invalid("mlp_hidden must be 32 or 64");
     if (c.n_controllers < 1) throw_invalid("n_controllers must be >= 1");
@@ -524,6 +527,23 @@ struct Handle final : HandleBase {
     invalidate_graphs();
   }
 
+  // BicycleParams::validate (dynamics.hpp:53-61) and the friction circle of
+  // brush_tire_force (dynamics.cpp:25-27) at the largest admissible throttle.
+  void set_bicycle(const mppi_bicycle_params& p) override {
+    if (cfg.system != MPPI_SYSTEM_VEHICLE_BICYCLE) throw_invalid("set_dynamics_bicycle: system is not the bicycle model");
+    const double v[9] = {p.mass, p.yaw_inertia, p.a, p.b, p.stiffness, p.mu, p.load, p.steer_scale, p.force_scale};
+    for (double x : v)
+      if (!(x > 0.0) || !std::isfinite(x)) throw_invalid("BicycleParams: all parameters must be positive");
+    const double thr = std::max(std::abs(cfg.bounds_lower[1]), std::abs(cfg.bounds_upper[1]));
+    if (p.force_scale * thr > p.mu * p.load)
+      throw Error(MPPI_ERR_DOMAIN, "brush_tire_force: |u_F| exceeds the friction circle mu*F_z");
+    bike_r = BicycleDev<R>{static_cast<R>(p.mass), static_cast<R>(p.yaw_inertia), static_cast<R>(p.a),
+                           static_cast<R>(p.b), static_cast<R>(p.stiffness), static_cast<R>(p.mu),
+                           static_cast<R>(p.load), static_cast<R>(p.steer_scale), static_cast<R>(p.force_scale)};
+    has_mlp = true;  // the model is set
+    invalidate_graphs();
+  }
+
   template <class Src>
   void set_map(int ctrl, const Src* values, int width, int height, double x0, double y0, double res) {
     if (cfg.system == MPPI_SYSTEM_QUADRATIC) throw_invalid("set_costmap: system has no costmap");
@@ -588,6 +608,14 @@ struct Handle final : HandleBase {
     invalidate_graphs();
   }
 
+  void map_geometry(int* w, int* h, double* x0, double* y0, double* res) const override {
+    if (!has_map) throw_invalid("costmap not set");
+    *w = map_w;
+    *h = map_h;
+    *x0 = map_x0;
+    *y0 = map_y0;
+    *res = map_res;
+  }
   void get_map_f32(int ctrl, float* out) override {
     check_ctrl(ctrl);
     if (!has_map) throw_invalid("get_costmap: no costmap set");
@@ -712,6 +740,7 @@ struct Handle final : HandleBase {
     s.with_terminal = cfg.with_terminal;
     s.quad_cost_scale = static_cast<R>(cfg.quad_cost_scale);
     s.theta = theta_r;
+    s.bike = bike_r;
     return s;
   }
   template <int HH>
@@ -742,6 +771,8 @@ struct Handle final : HandleBase {
       by_mode(std::integral_constant<int, 32>{}, type_tag<Quadratic<R, 32>>{});
     else if (cfg.system == MPPI_SYSTEM_VEHICLE_BASIS)
       by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleBasis<R, 32>>{});
+    else if (cfg.system == MPPI_SYSTEM_VEHICLE_BICYCLE)
+      by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleBicycle<R, 32>>{});
     else if (H == 32)
       by_mode(std::integral_constant<int, 32>{}, type_tag<VehicleMlp<R, 32>>{});
     else

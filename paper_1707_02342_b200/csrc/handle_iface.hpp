@@ -19,10 +19,12 @@ struct HandleBase {
   virtual void set_mlp(int hidden, const double* w1, const double* b1, const double* w2,
                        const double* b2, const double* w3, const double* b3) = 0;
   virtual void set_basis(const double* theta) = 0;
+  virtual void set_bicycle(const mppi_bicycle_params& p) = 0;
   virtual void set_map_f64(int ctrl, const double* v, int w, int h, double x0, double y0, double res) = 0;
   virtual void set_map_f32(int ctrl, const float* v, int w, int h, double x0, double y0, double res) = 0;
   virtual void perturb_fleet(double sigma, uint64_t seed) = 0;
   virtual void get_map_f32(int ctrl, float* out) = 0;
+  virtual void map_geometry(int* w, int* h, double* x0, double* y0, double* res) const = 0;
   virtual void set_plan(int ctrl, const double* U) = 0;
   virtual void get_plan(int ctrl, double* U) = 0;
   virtual void set_iteration(int ctrl, uint64_t it) = 0;

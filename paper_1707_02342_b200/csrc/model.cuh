@@ -225,6 +225,69 @@ __device__ __forceinline__ void eval_basis(R roll, R v_x, R v_y, R r, R u_delta,
   phi[24] = mul_rn(mul_rn(u_F, u_F), u_F);
 }
 
+// BicycleParams (dynamics.hpp:42-62).
+template <class R>
+struct BicycleDev {
+  R mass, yaw_inertia, a, b, stiffness, mu, load, steer_scale, force_scale;
+};
+
+// brush_tire_force (dynamics.cpp:23-43), the reference's expression order.
+// The |u_F| > mu F_z domain error is excluded once on the host (the throttle
+// is clamped to its bounds before the model, mppi_gpu_set_dynamics_bicycle);
+// a NaN here would surface as a non-finite cost.
+template <class R>
+__device__ __forceinline__ R brush_tire_force(R alpha, R u_F, const BicycleDev<R>& p) {
+  const R limit = mul_rn(p.mu, p.load);
+  if (abs_r(u_F) > limit) return R(NAN);
+  const R xi = div_r(sqrt_r(sub_rn(mul_rn(limit, limit), mul_rn(u_F, u_F))), limit);
+  if (xi == R(0)) return R(0);
+  const R sign = (alpha >= R(0)) ? R(1) : R(-1);
+  const R crossover = atan_r(div_r(mul_rn(mul_rn(mul_rn(R(3), xi), p.mu), p.load), p.stiffness));
+  if (abs_r(alpha) >= crossover) return mul_rn(mul_rn(mul_rn(-p.mu, xi), p.load), sign);
+  const R ta = tan_r(alpha);
+  const R c = p.stiffness;
+  const R t1 = mul_rn(-c, ta);
+  const R t2 = mul_rn(mul_rn(div_r(mul_rn(c, c), mul_rn(mul_rn(mul_rn(R(3), xi), p.mu), p.load)), ta), abs_r(ta));
+  // 27 mu mu xi xi load load, multiplied left to right as in the reference
+  const R den3 = mul_rn(mul_rn(mul_rn(mul_rn(mul_rn(mul_rn(R(27), p.mu), p.mu), xi), xi), p.load), p.load);
+  const R t3 = mul_rn(mul_rn(mul_rn(div_r(mul_rn(mul_rn(c, c), c), den3), ta), ta), ta);
+  return sub_rn(add_rn(t1, t2), t3);
+}
+
+// step_bicycle_truth (dynamics.cpp:51-81) on the 7-state (roll unchanged),
+// kSlipGuardSpeed = 0.1 (dynamics.cpp:47); v is the applied (clamped) input.
+template <class R>
+__device__ __forceinline__ void step_bicycle(R x[7], R steer, R throttle, R dt, const BicycleDev<R>& p) {
+  const R u_delta = mul_rn(p.steer_scale, steer);
+  const R u_F = mul_rn(p.force_scale, throttle);
+  const R r = x[6];
+  R alpha_f, alpha_r;
+  if (x[4] > R(0.1)) {
+    const R beta = div_r(x[5], x[4]);
+    alpha_f = sub_rn(atan_r(add_rn(beta, div_r(mul_rn(p.a, r), x[4]))), u_delta);
+    alpha_r = atan_r(sub_rn(beta, div_r(mul_rn(p.b, r), x[4])));
+  } else {
+    alpha_f = -u_delta;
+    alpha_r = R(0);
+  }
+  const R f_yf = brush_tire_force<R>(alpha_f, u_F, p);
+  const R f_yr = brush_tire_force<R>(alpha_r, u_F, p);
+  R s, c;
+  sincos_r(x[2], &s, &c);
+  const R n0 = add_rn(x[0], mul_rn(sub_rn(mul_rn(c, x[4]), mul_rn(s, x[5])), dt));
+  const R n1 = add_rn(x[1], mul_rn(add_rn(mul_rn(s, x[4]), mul_rn(c, x[5])), dt));
+  const R n2 = add_rn(x[2], mul_rn(r, dt));
+  const R n4 = add_rn(x[4], mul_rn(add_rn(div_r(sub_rn(u_F, mul_rn(f_yf, sin_r(u_delta))), p.mass), mul_rn(r, x[5])), dt));
+  const R n5 = add_rn(x[5], mul_rn(sub_rn(div_r(add_rn(f_yf, f_yr), p.mass), mul_rn(r, x[4])), dt));
+  const R n6 = add_rn(x[6], mul_rn(div_r(sub_rn(mul_rn(p.a, f_yf), mul_rn(p.b, f_yr)), p.yaw_inertia), dt));
+  x[0] = n0;
+  x[1] = n1;
+  x[2] = n2;
+  x[4] = n4;
+  x[5] = n5;
+  x[6] = n6;
+}
+
 // Everything a rollout system needs besides the weights.
 template <class R>
 struct SystemArgs {
@@ -235,6 +298,7 @@ struct SystemArgs {
   int with_terminal;
   R quad_cost_scale;
   ThetaDev<R> theta;     // VEHICLE_BASIS coefficients
+  BicycleDev<R> bike;    // VEHICLE_BICYCLE parameters
 };
 
 template <class R, int H>
@@ -273,6 +337,17 @@ struct VehicleBasis {
       d[o] = acc;
     }
     advance_split<R>(x, d, a.dt);
+  }
+};
+
+// make_vehicle_system over BicycleTruthModel: clamp -> step_bicycle_truth.
+template <class R, int H>
+struct VehicleBicycle {
+  static constexpr int kStateDim = 7;
+  static constexpr bool kHasMap = true;
+  static constexpr bool kMlp = false;
+  __device__ __forceinline__ static void step(R x[7], R v0, R v1, const MlpParams<R, H>&, const SystemArgs<R>& a) {
+    step_bicycle<R>(x, clamp_r(v0, a.lo0, a.hi0), clamp_r(v1, a.lo1, a.hi1), a.dt, a.bike);
   }
 };
 

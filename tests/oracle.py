@@ -48,6 +48,9 @@ _SIG = {
     "oracle_set_mlp": (c_int, [c_void_p, c_int, _d, _d, _d, _d, _d, _d]),
     "oracle_set_costmap": (c_int, [c_void_p, _d, c_int, c_int, c_double, c_double, c_double]),
     "oracle_set_theta": (c_int, [c_void_p, _d]),
+    "oracle_set_bicycle": (c_int, [c_void_p, _d]),
+    "oracle_brush_tire_force": (c_int, [c_double, c_double, _d, _d]),
+    "oracle_step_bicycle": (c_int, [_d, _d, c_double, _d, _d]),
     "oracle_eval_basis": (c_int, [_d, _d, _d]),
     "oracle_step_basis": (c_int, [_d, _d, c_double, _d, _d]),
     "oracle_set_costmap_f32": (c_int, [c_void_p, POINTER(c_float), c_int, c_int, c_double, c_double, c_double]),
@@ -233,6 +236,12 @@ class OracleController:
     def set_mlp(self, w):
         arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (w.w1, w.b1, w.w2, w.b2, w.w3, w.b3)]
         chk(load().oracle_set_mlp(self.h, w.hidden, *[p(a) for a in arrs]))
+
+    def set_bicycle(self, params=None):
+        from paper_1707_02342_b200.api import BicycleParams
+        b = params or BicycleParams()
+        v = np.array([getattr(b, f) for f in BicycleParams.__dataclass_fields__], dtype=np.float64)
+        chk(load().oracle_set_bicycle(self.h, p(v)))
 
     def set_basis(self, theta):
         t = np.ascontiguousarray(theta, dtype=np.float64).reshape(25, 4)
