@@ -76,6 +76,26 @@ int main() {
     threw = true;
   }
   EXPECT(threw);
+  // sizes are checked before the C ABI reads K / 2T / state_dim entries
+  auto throws_invalid = [](auto&& f) {
+    try {
+      f();
+    } catch (const std::invalid_argument&) {
+      return true;
+    }
+    return false;
+  };
+  EXPECT(throws_invalid([&] { ctl.compute_weights(std::vector<double>(63, 1.0)); }));
+  EXPECT(throws_invalid([&] {
+    mppi::gpu::WeightResult short_w;
+    short_w.weights.assign(10, 0.1);
+    ctl.update_plan(short_w);
+  }));
+  EXPECT(throws_invalid([&] { ctl.set_plan(std::vector<double>(3, 0.0)); }));
+  EXPECT(throws_invalid([&] { ctl.mpc_step(std::vector<double>(7, 0.0)); }));
+  EXPECT(throws_invalid([&] { ctl.rollout_batch(std::vector<double>(1, 0.0)); }));
+  EXPECT(ctl.iteration() == 1);  // none of the rejected calls touched the state
+  std::printf("size checks ok\n");
   std::printf("device binding ok: u0 = (%g, %g)\n", u0[0], u0[1]);
   return fails ? 1 : 0;
 }

@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "mppi_gpu.h")
 def declared_symbols():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b((?:mppi_gpu|mppi_workload|mppi_sg)_\w+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b((?:mppi_gpu|mppi_workload|mppi_sg|mppi_sim|mppi_bicycle|mppi_brush)_\w+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -132,4 +132,4 @@ def test_cpp_binding_exception_mapping(tmp_path):
 def test_cpp_binding_on_device(tmp_path):
     out = subprocess.run([build_binding_check(str(tmp_path))], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "device binding ok" in out.stdout
+    assert "device binding ok" in out.stdout and "size checks ok" in out.stdout
