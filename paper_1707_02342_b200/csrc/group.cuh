@@ -31,6 +31,7 @@ namespace mppi_dev {
 constexpr int kGroupStripes = 8;    // warps per CTA; stripe q sums rows q, q + 8, ...
 constexpr int kGroupElems = 32;     // elements per CTA (one per lane)
 constexpr int kGroupBlock = 32 * kGroupStripes;
+static_assert(kGroupRowsMax % kGroupStripes == 0 && kGroupRowsMax <= kGroupBlock, "group shape");
 
 // grid = (groups of this rank, ceil(stride / kGroupElems), controllers),
 // block = kGroupBlock.  partials: [C][n_chunks][stride] (global chunk index);
@@ -54,6 +55,16 @@ __global__ void __launch_bounds__(kGroupBlock) group_merge_kernel(const Acc* __r
   const int n = r1 - r0;  // <= kGroupRowsMax (0: an empty group, K < 8 chunks)
   const Acc* P = partials + static_cast<size_t>(ctrl) * partials_ctrl_stride + static_cast<size_t>(r0) * stride;
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int e = blockIdx.y * kGroupElems + lane;
+  // this lane's element of its stripe's rows (q, q + 8, ...), all loads in
+  // flight at once, issued before the group minimum is known
+  constexpr int kPer = kGroupRowsMax / kGroupStripes;
+  Acc v[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int r = q + kGroupStripes * i;
+    v[i] = (r < n && e < stride) ? __ldcg(P + static_cast<size_t>(r) * stride + e) : 0.0;
+  }
   // rho_g = min over the group's chunk minima; bad_g = any chunk non-finite
   Acc m = INFINITY;
   int bad = 0;
@@ -74,12 +85,11 @@ __global__ void __launch_bounds__(kGroupBlock) group_merge_kernel(const Acc* __r
   const double inv_lambda = 1.0 / lambda;
   if (threadIdx.x < n) s_scale[threadIdx.x] = exp(-(s_scale[threadIdx.x] - rho) * inv_lambda);
   __syncthreads();
-  const int e = blockIdx.y * kGroupElems + lane;
   Acc s = 0.0;
-  if (e < stride) {
-    const Acc* pe = P + e;
-#pragma unroll 4
-    for (int r = q; r < n; r += kGroupStripes) s = fma(s_scale[r], __ldcg(pe + static_cast<size_t>(r) * stride), s);
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int r = q + kGroupStripes * i;
+    if (r < n) s = fma(s_scale[r], v[i], s);
   }
   s_part[q][lane] = s;
   __syncthreads();

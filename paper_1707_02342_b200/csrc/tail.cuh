@@ -147,42 +147,44 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
     }
   }
   if (a.plant) {
+    // the plant step of the same MLP by warp 0: lane j owns hidden units
+    // j, j + 32, ...; activations go through shared memory (broadcast reads,
+    // so every FMA chain has its operands without a shuffle round trip);
+    // per unit the operation order is that of epilogue_kernel
+    __shared__ float s_h[2 * H];
+    __shared__ float s_d[4];
     const MlpParams<float, H>& w = *s_w;
     float x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = s_x[i];
     const float in[6] = {x[3], x[4], x[5], x[6], u0, u1};
-    float h1[U], h2[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = lane + 32 * u;
       float acc = w.b1[j];
 #pragma unroll
       for (int i = 0; i < 6; ++i) acc = fma_r(w.w1t[i][j], in[i], acc);
-      h1[u] = tanh_r(acc);
+      s_h[j] = tanh_r(acc);
     }
+    __syncwarp();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = lane + 32 * u;
       float acc = w.b2[j];
-#pragma unroll
-      for (int uu = 0; uu < U; ++uu)
-#pragma unroll 8
-        for (int i = 0; i < 32; ++i) acc = fma_r(w.w2t[32 * uu + i][j], __shfl_sync(0xffffffffu, h1[uu], i), acc);
-      h2[u] = tanh_r(acc);
+#pragma unroll 16
+      for (int i = 0; i < H; ++i) acc = fma_r(w.w2t[i][j], s_h[i], acc);
+      s_h[H + j] = tanh_r(acc);
     }
-    float d = (lane < 4) ? w.b3[lane] : 0.f;
-#pragma unroll
-    for (int uu = 0; uu < U; ++uu)
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const float hi = __shfl_sync(0xffffffffu, h2[uu], i);
-        if (lane < 4) d = fma_r(w.w3t[32 * uu + i][lane], hi, d);
-      }
-    float dd[4];
-#pragma unroll
-    for (int o = 0; o < 4; ++o) dd[o] = __shfl_sync(0xffffffffu, d, o);
+    __syncwarp();
+    if (lane < 4) {
+      float d = w.b3[lane];
+#pragma unroll 16
+      for (int i = 0; i < H; ++i) d = fma_r(w.w3t[i][lane], s_h[H + i], d);
+      s_d[lane] = d;
+    }
+    __syncwarp();
     if (lane == 0) {
+      float dd[4] = {s_d[0], s_d[1], s_d[2], s_d[3]};
       advance_split<float>(x, dd, a.sys.dt);
       float* xo = a.x0 + static_cast<size_t>(ctrl) * 8;
       for (int i = 0; i < 7; ++i) xo[i] = x[i];
