@@ -3,10 +3,30 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <type_traits>
 
 namespace mppi_dev {
+
+// Device-side invariant checks of a debug build (-DMPPI_DEVICE_CHECKS): every
+// global write of the hot path checks its index against the buffer it owns
+// and traps otherwise (compute-sanitizer is not available on the GPU pool;
+// tools/gpu_device_checks.sh runs the GPU tests on this build).
+#ifdef MPPI_DEVICE_CHECKS
+#define MPPI_DCHECK(cond)                                                                         \
+  do {                                                                                            \
+    if (!(cond)) {                                                                                \
+      printf("MPPI_DCHECK failed %s:%d block (%d,%d,%d) thread %d: %s\n", __FILE__, __LINE__,     \
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, #cond);                             \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define MPPI_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 // Rounded (never contracted) arithmetic.  The state update and the cost use
 // these so the fp32/fp64 device paths perform the same operation sequence as

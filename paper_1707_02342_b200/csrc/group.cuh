@@ -53,6 +53,8 @@ __global__ void __launch_bounds__(kGroupBlock) group_merge_kernel(const Acc* __r
   const int g = g0 + blockIdx.x, ctrl = blockIdx.z;
   const int r0 = group_first_chunk(g, n_chunks, n_groups), r1 = group_first_chunk(g + 1, n_chunks, n_groups);
   const int n = r1 - r0;  // <= kGroupRowsMax (0: an empty group, K < 8 chunks)
+  MPPI_DCHECK(g < n_groups && n >= 0 && n <= kGroupRowsMax && r1 <= n_chunks);
+  MPPI_DCHECK(static_cast<long long>(r1) * stride <= partials_ctrl_stride);
   const Acc* P = partials + static_cast<size_t>(ctrl) * partials_ctrl_stride + static_cast<size_t>(r0) * stride;
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
   const int e = blockIdx.y * kGroupElems + lane;

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(BLOCK) rollout_kernel(const __grid_constant__ 
   __syncthreads();
   Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
              static_cast<size_t>(chunk) * a.partial_stride;
+  MPPI_DCHECK(static_cast<long long>(chunk + 1) * a.partial_stride <= a.partials_ctrl_stride);
   for (int i = threadIdx.x; i < 2 * T; i += BLOCK) {
     Acc s = s_num[i];
 #pragma unroll

@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     e0 = zm ? e0 - u0 : e0;
     e1 = zm ? e1 - u1 : e1;
     if constexpr (STORE) {
-      if (t < T) s_eps[t * CH + s_own] = make_float2(e0, e1);  // mirrors store identical values
+      if (t < T && !dup) s_eps[t * CH + s_own] = make_float2(e0, e1);  // owners only (predicated)
     }
     const float v0 = u0 + e0, v1 = u1 + e1;
     const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
@@ -509,22 +509,25 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx), mul_rn(cs, vy)), dt));
     th = add_rn(th, mul_rn(thd, dt));
     const MapTaps<float> q_next = map_fetch(map, px, py);
-    // stage this step's inputs (owner; MT = 1 mirror lanes store the same
-    // values to the same row, so no branch splits the step's basic block)
+    // stage this step's inputs (the owners' predicated stores: the MT = 1
+    // mirror lanes compute the same values and store nothing, so no two
+    // lanes write one word and no branch splits the step's basic block)
     {
       uint32_t* hi_plane = st.in[m_own][0];
       uint32_t* lo_plane = st.in[m_own][1];
       const int h = t4 & 1;
-      uint32_t hi, lo;
-      split2(roll, vx, hi, lo);
-      hi_plane[tc_in_word(g, 0, h)] = hi;
-      lo_plane[tc_in_word(g, 0, h)] = lo;
-      split2(vy, thd, hi, lo);
-      hi_plane[tc_in_word(g, 1, h)] = hi;
-      lo_plane[tc_in_word(g, 1, h)] = lo;
-      split2(v0c, v1c, hi, lo);
-      hi_plane[tc_in_word(g, 2, h)] = hi;
-      lo_plane[tc_in_word(g, 2, h)] = lo;
+      uint32_t hi0, lo0, hi1, lo1, hi2, lo2;
+      split2(roll, vx, hi0, lo0);
+      split2(vy, thd, hi1, lo1);
+      split2(v0c, v1c, hi2, lo2);
+      if (!dup) {
+        hi_plane[tc_in_word(g, 0, h)] = hi0;
+        lo_plane[tc_in_word(g, 0, h)] = lo0;
+        hi_plane[tc_in_word(g, 1, h)] = hi1;
+        lo_plane[tc_in_word(g, 1, h)] = lo1;
+        hi_plane[tc_in_word(g, 2, h)] = hi2;
+        lo_plane[tc_in_word(g, 2, h)] = lo2;
+      }
     }
     __syncwarp();
     float d3[MT][4];
@@ -575,6 +578,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
     cost += static_cast<Acc>(add_rn(tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[T - 1], cp), p_coup));
     if (a.sys.with_terminal) cost += static_cast<Acc>(tc_state_cost<STAB>(h, p_roll, p_vx, p_vy, a.sys.decay_pow[T], cp));
   }
+  MPPI_DCHECK(!valid || (k >= 0 && k < a.K));
   if (valid) a.costs[static_cast<size_t>(ctrl) * a.K + k] = cost;
   const bool bad = valid && !isfinite(cost);
   const Acc rho = warp_min(valid ? cost : Acc(INFINITY));
@@ -583,6 +587,9 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
   Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
              static_cast<size_t>(chunk) * a.partial_stride;
+  MPPI_DCHECK(!active || (chunk >= a.chunk0 && static_cast<long long>(chunk + 1) * a.partial_stride <=
+                                                    a.partials_ctrl_stride));
+  MPPI_DCHECK(a.partial_stride == kPartialHeader + 2 * T);
   if (lane == 0 && active) {
     out[0] = rho;
     out[1] = eta;

@@ -139,19 +139,22 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
     const float u0 = s_plan[2 * t], u1 = s_plan[2 * t + 1];
     e0 = zm ? e0 - u0 : e0;
     e1 = zm ? e1 - u1 : e1;
-    s_eps[t * 16 + row_own] = make_float2(e0, e1);  // mirrors store identical values
+    if (!dup) s_eps[t * 16 + row_own] = make_float2(e0, e1);  // owners only (predicated)
     const float v0 = u0 + e0, v1 = u1 + e1;
     const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
     const float uu = __fmul_rn(__fmul_rn(u0, u0), inv_s0) + __fmul_rn(__fmul_rn(u1, u1), inv_s1);
-    s_coup[t * 16 + row_own] = zm ? __fadd_rn(__fmul_rn(gml, uv), __fmul_rn(half_lambda, uu)) : __fmul_rn(a.gamma, uv);
+    const float coup = zm ? __fadd_rn(__fmul_rn(gml, uv), __fmul_rn(half_lambda, uu)) : __fmul_rn(a.gamma, uv);
+    if (!dup) s_coup[t * 16 + row_own] = coup;
     v0c = clamp_r(v0, a.sys.lo0, a.sys.hi0);
     v1c = clamp_r(v1, a.sys.lo1, a.sys.hi1);
   };
   auto stage_v = [&] {
     uint32_t hi, lo;
     split2(v0c, v1c, hi, lo);
-    st.in[0][tc_in_word(g, 2, hrow)] = hi;
-    st.in[1][tc_in_word(g, 2, hrow)] = lo;
+    if (!dup) {
+      st.in[0][tc_in_word(g, 2, hrow)] = hi;
+      st.in[1][tc_in_word(g, 2, hrow)] = lo;
+    }
   };
 
   // ---- state warp: the 7-state, costmap taps, cost
@@ -187,13 +190,15 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
       py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx), mul_rn(cs, vy)), dt));
       th = add_rn(th, mul_rn(thd, dt));
       q_next = map_fetch(map, px, py);
-      uint32_t hi, lo;
-      split2(roll, vx, hi, lo);
-      st.in[0][tc_in_word(g, 0, hrow)] = hi;
-      st.in[1][tc_in_word(g, 0, hrow)] = lo;
-      split2(vy, thd, hi, lo);
-      st.in[0][tc_in_word(g, 1, hrow)] = hi;
-      st.in[1][tc_in_word(g, 1, hrow)] = lo;
+      uint32_t hi0, lo0, hi1, lo1;
+      split2(roll, vx, hi0, lo0);
+      split2(vy, thd, hi1, lo1);
+      if (!dup) {  // owners only (predicated): no two lanes write one word
+        st.in[0][tc_in_word(g, 0, hrow)] = hi0;
+        st.in[1][tc_in_word(g, 0, hrow)] = lo0;
+        st.in[0][tc_in_word(g, 1, hrow)] = hi1;
+        st.in[1][tc_in_word(g, 1, hrow)] = lo1;
+      }
     }
     tc_pair_bar(bar_id);  // (1) inputs of step t staged
     // ---- layer 1, this warp's two n-tiles (as tc_mlp)
@@ -321,6 +326,8 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
   // ---- terminal cost and the chunk softmin partials (state warp)
   Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
              static_cast<size_t>(chunk) * a.partial_stride;
+  MPPI_DCHECK(!active || static_cast<long long>(chunk + 1) * a.partial_stride <= a.partials_ctrl_stride);
+  MPPI_DCHECK(!valid || k < a.K);
   if (half == 0) {
     const float h = map_interp(q);
     cost += static_cast<Acc>(

@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
   tail_prefetch<H>(ta.e, static_cast<const MlpParams<float, H>*>(ta.plant_w), ctrl, pre);
   cudaGridDependencySynchronize();  // everything below reads the group rows
   const Acc* P = rows + static_cast<size_t>(ctrl) * ctrl_stride;
+  MPPI_DCHECK(static_cast<long long>(n) * stride <= ctrl_stride && stride == kPartialHeader + 2 * T);
   // rho = min over the group rows, bad = any group non-finite
   Acc m = INFINITY;
   int bad = 0;
