@@ -74,6 +74,27 @@ __device__ __forceinline__ R clamp_r(R v, R lo, R hi) {
   return (v < lo) ? lo : ((hi < v) ? hi : v);
 }
 
+// Timeline stamps of a profiling build (-DMPPI_STAMPS): %globaltimer at the
+// phase boundaries of one iteration (K1 end, group merge, tail phases),
+// printed by the tail.  Slot i holds the max (ends) or min (starts) over CTAs.
+#ifdef MPPI_STAMPS
+__device__ unsigned long long g_stamps[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MPPI_STAMP_MAX(i) atomicMax(&::mppi_dev::g_stamps[i], ::mppi_dev::gtimer())
+#define MPPI_STAMP_MIN(i) atomicMin(&::mppi_dev::g_stamps[i], ::mppi_dev::gtimer())
+#else
+#define MPPI_STAMP_MAX(i) \
+  do {                    \
+  } while (0)
+#define MPPI_STAMP_MIN(i) \
+  do {                    \
+  } while (0)
+#endif
+
 template <class R>
 __device__ __forceinline__ R warp_sum(R v) {
 #pragma unroll

@@ -47,9 +47,11 @@ __global__ void __launch_bounds__(kGroupBlock) group_merge_kernel(const Acc* __r
   __shared__ Acc s_scale[kGroupRowsMax];
   __shared__ Acc s_part[kGroupStripes][kGroupElems];
   __shared__ Acc s_min[kGroupStripes];
-  cudaGridDependencySynchronize();
-  // the tail (a programmatic dependent) may launch and stage its inputs now
+  // the tail (a programmatic dependent) may launch now and stage its inputs
+  // while K1 and this grid run; its own grid-dependency wait still covers
+  // this grid's completion
   cudaTriggerProgrammaticLaunchCompletion();
+  cudaGridDependencySynchronize();
   const int g = g0 + blockIdx.x, ctrl = blockIdx.z;
   const int r0 = group_first_chunk(g, n_chunks, n_groups), r1 = group_first_chunk(g + 1, n_chunks, n_groups);
   const int n = r1 - r0;  // <= kGroupRowsMax (0: an empty group, K < 8 chunks)
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(kGroupBlock) group_merge_kernel(const Acc* __r
     else if (e == 3) v = 0.0;
     groups[static_cast<size_t>(ctrl) * groups_ctrl_stride + static_cast<size_t>(g) * stride + e] = v;
   }
+
 }
 
 }  // namespace mppi_dev

@@ -590,6 +590,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   MPPI_DCHECK(!active || (chunk >= a.chunk0 && static_cast<long long>(chunk + 1) * a.partial_stride <=
                                                     a.partials_ctrl_stride));
   MPPI_DCHECK(a.partial_stride == kPartialHeader + 2 * T);
+  if (lane == 0) MPPI_STAMP_MAX(0);  // K1: last warp through the rollout
   if (lane == 0 && active) {
     out[0] = rho;
     out[1] = eta;

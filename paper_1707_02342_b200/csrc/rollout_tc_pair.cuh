@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
     const Acc wk = valid ? exp(-(cost - rho) / a.dlambda) : 0.0;
     const Acc eta = warp_sum(wk);
     const unsigned any_bad = __ballot_sync(0xffffffffu, bad);
+    if (lane == 0) MPPI_STAMP_MAX(0);  // K1: last state warp through the rollout
     if (lane == 0 && active) {
       out[0] = rho;
       out[1] = eta;

@@ -69,7 +69,7 @@ __device__ __forceinline__ void publish_status(const EpilogueArgs<float>& a, int
 
 template <int H>
 __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* s_row, int bad, int ctrl,
-                                              unsigned char* smem, const unsigned char* pre) {
+                                              unsigned char* smem, const unsigned char* pre, int code0, uint64_t it0) {
   constexpr int U = H / 32;  // hidden units per lane
   const int T = a.T;
   double* s_agg = reinterpret_cast<double*>(smem);
@@ -83,15 +83,16 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   for (int j = threadIdx.x; j < a.sg_window; j += kTailBlock) s_sg[j] = a.sg[j];
   StepStatus* st = a.status + ctrl;
   float* plan = a.plan + static_cast<size_t>(ctrl) * 2 * T;
-  // ---- phase 1: the merged row (shared memory) and the status (the rest was prefetched)
+  // ---- phase 1: the merged row (shared memory) and the status (prefetched
+  // before the grid dependency with the plan, the plant state and the weights)
   if (threadIdx.x == 0) {
-    int code = __ldcg(&st->code);
+    int code = code0;
     if (code == 0 && bad) code = 2;  // it_weights: non-finite cost (weights.cpp:12)
     s_code = code;
   }
-  const double eta_l = s_row[1];
+  const double inv_eta = 1.0 / s_row[1];
   for (int i = threadIdx.x; i < 2 * T; i += kTailBlock)
-    s_agg[i] = s_row[kPartialHeader + i] / eta_l;  // agg = num / eta, once per element
+    s_agg[i] = s_row[kPartialHeader + i] * inv_eta;  // agg = num / eta
   __syncthreads();
   if (s_code != 0) {
     if (threadIdx.x == 0) {
@@ -133,8 +134,9 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   const float u0 = clamp_r(s_new[0], a.lo0, a.hi0), u1 = clamp_r(s_new[1], a.lo1, a.hi1);
   for (int i = threadIdx.x; i < 2 * T; i += kTailBlock)
     plan[i] = a.slide ? ((i + 2 < 2 * T) ? s_new[i + 2] : 0.f) : s_new[i];
-  uint64_t it = a.iters[ctrl];
+  uint64_t it = it0;
   if (a.increment) it += 1;
+  if (threadIdx.x == 0) MPPI_STAMP_MIN(5);  // SG + U' + plan written (thread 0)
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   if (lane == 0) {
@@ -195,6 +197,7 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
       }
     }
   }
+  if (lane == 0) MPPI_STAMP_MIN(6);  // plant done
   if (lane == 0) {
     a.iters[ctrl] = it;
     st->iteration = it;
@@ -225,7 +228,12 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
   // plan, plant state and weights are not written by the group merge: fetch
   // them while it may still be running (this kernel is its programmatic dependent)
   tail_prefetch<H>(ta.e, static_cast<const MlpParams<float, H>*>(ta.plant_w), ctrl, pre);
+  // the sticky status and the iteration counter are not written by K1 or the
+  // group merge either (a failed step clears the status before the next one)
+  const int code0 = (threadIdx.x == 0) ? __ldcg(&ta.e.status[ctrl].code) : 0;
+  const uint64_t it0 = ta.e.iters[ctrl];
   cudaGridDependencySynchronize();  // everything below reads the group rows
+  if (threadIdx.x == 0) MPPI_STAMP_MIN(3);
   const Acc* P = rows + static_cast<size_t>(ctrl) * ctrl_stride;
   MPPI_DCHECK(static_cast<long long>(n) * stride <= ctrl_stride && stride == kPartialHeader + 2 * T);
   // rho = min over the group rows, bad = any group non-finite
@@ -240,12 +248,14 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
   m = warp_min(m);
   if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = m;
   bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) MPPI_STAMP_MIN(7);  // group minima loaded
   Acc rho = s_min[0];
 #pragma unroll
   for (int w = 1; w < kTailBlock / 32; ++w) rho = (s_min[w] < rho) ? s_min[w] : rho;
   const double inv_lambda = 1.0 / lambda;
   for (int r = threadIdx.x; r < n; r += kTailBlock) s_scale[r] = exp(-(s_scale[r] - rho) * inv_lambda);
   __syncthreads();
+  if (threadIdx.x == 0) MPPI_STAMP_MIN(8);  // scales
   // merged element e (eta and the numerators): the rows in group order
   for (int e = threadIdx.x; e < stride; e += kTailBlock) {
     if (e == 1 || e >= kPartialHeader) {
@@ -257,7 +267,20 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
     }
   }
   __syncthreads();
-  epilogue_fast<H>(ta.e, s_row, bad, ctrl, epi, pre);
+  if (threadIdx.x == 0) MPPI_STAMP_MIN(4);  // merged row in shared memory
+  epilogue_fast<H>(ta.e, s_row, bad, ctrl, epi, pre, code0, it0);
+#ifdef MPPI_STAMPS
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* s = g_stamps;
+    const unsigned long long e = gtimer();
+    printf("STAMPS k1_end->tail_start %lld rho_loads %lld scales %lld elements %lld sg_plan %lld plant %lld status %lld ns\n",
+           static_cast<long long>(s[3] - s[0]), static_cast<long long>(s[7] - s[3]),
+           static_cast<long long>(s[8] - s[7]), static_cast<long long>(s[4] - s[8]),
+           static_cast<long long>(s[5] - s[4]), static_cast<long long>(s[6] - s[5]), static_cast<long long>(e - s[6]));
+    s[0] = 0;
+    s[3] = ~0ull; s[4] = ~0ull; s[5] = ~0ull; s[6] = ~0ull; s[7] = ~0ull; s[8] = ~0ull;
+  }
+#endif
 }
 
 }  // namespace mppi_dev
