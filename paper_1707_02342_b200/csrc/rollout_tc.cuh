@@ -259,6 +259,9 @@ struct TcStage {
 };
 constexpr int kTcTB = 16;  // timesteps per block of the numerator reduction
 constexpr int kTcRedStride = 33;  // doubles per row (padding: conflict-free column reads)
+// doubles of numerator scratch per warp: the staged reduction of regenerated
+// eps', or the chunk's 16 softmin weights when eps' is on chip
+__host__ __device__ constexpr int tc_red_doubles(bool store) { return store ? 16 : 2 * kTcTB * kTcRedStride; }
 
 // MLP of one step for MT tiles: inputs from the stage, outputs d3 (fp32).
 // side1 / side2: independent per-sample work of the step, placed between the
@@ -344,8 +347,17 @@ __device__ __forceinline__ void tc_mlp(const TcStage<MT>& st, int g, int t4, con
 // grid = (ceil(chunks / NW), controllers), block = 32 * NW; one warp = one
 // chunk of 16*MT samples.  Dynamic smem: plan (2T + 2 floats), then the
 // numerator reduction buffers (NW x 2*kTcTB x kTcRedStride doubles).
+// Resident CTAs per SM the register budget is sized for (measured,
+// profiles/README.md): MT = 2 three (168 registers; four spills); MT = 1 at
+// H = 32 three (158 registers, no spills: the group-merge CTAs of the
+// programmatic-dependent launch then fit beside two K1 CTAs, c1 -1.3 %);
+// H = 64 two (its layer-2 chain needs the registers: three is +8 % at c2).
+template <int H, int MT>
+__host__ __device__ constexpr int tc_min_ctas() {
+  return (MT == 2 || H == 32) ? 3 : 2;
+}
 template <int H, int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
-__global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
+__global__ void __launch_bounds__(32 * NW, tc_min_ctas<H, MT>()) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const uint32_t* __restrict__ frag) {
   constexpr int CH = 16 * MT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // its samples on chip, [warp][t][sample] float2, for the numerator pass —
   // used when the whole grid fits one wave with this footprint (small K);
   // otherwise eps' is regenerated from the counters.
-  float2* s_eps_all = reinterpret_cast<float2*>(s_red_all + static_cast<size_t>(NW) * 2 * kTcTB * kTcRedStride);
+  float2* s_eps_all = reinterpret_cast<float2*>(s_red_all + static_cast<size_t>(NW) * tc_red_doubles(STORE));
   __shared__ __align__(16) TcStage<MT> s_stage[NW];
 
   const int ctrl = blockIdx.y;
@@ -600,7 +612,7 @@ __global__ void __launch_bounds__(32 * NW, (MT == 2 ? 3 : 2)) rollout_tc_kernel(
   // numerators over the regenerated batch (eps' = eps - U for zero-mean):
   // blocks of kTcTB steps, products staged [t][c][lane] in shared memory and
   // summed per (t, c) over the lanes in ascending lane order by one lane each.
-  double* red = s_red_all + static_cast<size_t>(warp) * (2 * kTcTB) * kTcRedStride;
+  double* red = s_red_all + static_cast<size_t>(warp) * tc_red_doubles(STORE);
   if constexpr (STORE && MT == 1) {
     // eps' is on chip: each lane sums whole (t, c) elements over the chunk's
     // rows with the staged reduction's order below (rows 0..7 and rows 8..15

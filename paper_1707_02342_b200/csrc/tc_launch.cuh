@@ -74,12 +74,14 @@ cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
   return cudaGetLastError();
 }
 // eps' stays on chip when the grid still fits one wave with that footprint
-// (2 CTAs of 4 warps per SM); larger launches regenerate it from the counters.
+// (tc_min_ctas CTAs of 4 warps per SM); larger launches regenerate it from
+// the counters.
 template <int H, int MT, int Mode, bool STAB>
 cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
                cudaStream_t stream) {
   const size_t plan_bytes = (sizeof(float) * (2 * a.T + 2) + 15) & ~size_t(15);
-  const size_t base = plan_bytes + sizeof(double) * kTcWarps * 2 * mppi_dev::kTcTB * mppi_dev::kTcRedStride;
+  const size_t base = plan_bytes + sizeof(double) * kTcWarps * mppi_dev::tc_red_doubles(false);
+  const size_t base_store = plan_bytes + sizeof(double) * kTcWarps * mppi_dev::tc_red_doubles(true);
   const size_t eps_bytes = sizeof(float2) * kTcWarps * a.T * 16 * MT;
   static int sms = [] {
     int dev = 0, n = 148;
@@ -88,8 +90,10 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int 
     return n;
   }();
   const long long ctas = static_cast<long long>((n_chunks + kTcWarps - 1) / kTcWarps) * ctrls;
+  constexpr int per_sm = mppi_dev::tc_min_ctas<H, MT>();
   const bool store = std::getenv("MPPI_TC_STORE") ? std::atoi(std::getenv("MPPI_TC_STORE")) != 0
-                                                   : (base + eps_bytes <= 110 * 1024 && ctas <= 2LL * sms);
+                                                   : (per_sm * (base_store + eps_bytes) <= 220 * 1024 &&
+                                                      ctas <= per_sm * static_cast<long long>(sms));
   g_tc_last_pair = 0;
   if constexpr (H == 32 && MT == 1) {
     if (!a.trace_states && pair_fits<Mode, STAB>(a.T, n_chunks, ctrls))
@@ -98,7 +102,7 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int 
   // (MT = 2 serves K > 32768, whose grid never fits one wave: no on-chip eps')
   if constexpr (MT == 1) {
     if (store && !a.trace_states)
-      return go_store<H, MT, Mode, STAB, true>(a, frag, n_chunks, ctrls, base + eps_bytes, stream);
+      return go_store<H, MT, Mode, STAB, true>(a, frag, n_chunks, ctrls, base_store + eps_bytes, stream);
   }
   return go_store<H, MT, Mode, STAB, false>(a, frag, n_chunks, ctrls, base, stream);
 }
