@@ -20,6 +20,9 @@ struct StepStatus {
   double u0[2];    // clamp(U'[0])
   double x[8];     // state after the device plant (closed loop)
   unsigned long long iteration;
+  // host mirror only: bumped after every other field of a step is published
+  // (the host waits on it instead of a stream synchronisation, handle.cuh)
+  unsigned long long seq;
 };
 
 constexpr int kMaxSgWindow = 63;

@@ -10,6 +10,8 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -228,6 +230,7 @@ struct Handle final : HandleBase {
   // tensor-core tail (tail.cuh): merge of the group rows + epilogue, one CTA per controller
   DevBuf<unsigned char> d_plantw;  // MlpParams<float, H> (the plant step of the tail)
   int graph_kernels[4] = {0, 0, 0, 0};
+  bool graph_direct[4] = {false, false, false, false};  // the graph's tail publishes the host status itself
   bool status_direct = false;      // capture in progress: the tail writes h_status itself
   // sample sharding: NCCL all-gather of the group rows, or (in one process)
   // peer copies from the other handles of a local group
@@ -267,6 +270,7 @@ struct Handle final : HandleBase {
   double map_x0 = 0, map_y0 = 0, map_res = 1;
   HostPinned<R> h_x0;
   HostPinned<StepStatus> h_status;
+  std::vector<unsigned long long> seq_want;
   std::vector<uint64_t> h_iters;
 
   // last parity batch (for update_plan / rollout_states)
@@ -343,6 +347,7 @@ struct Handle final : HandleBase {
     d_status.alloc(C);
     CUDA_TRY(cudaMemset(d_status.p, 0, C * sizeof(StepStatus)));
     h_status.alloc(C);
+    std::memset(h_status.p, 0, sizeof(StepStatus) * C);
     h_x0.alloc(static_cast<size_t>(C) * 8);
     std::memset(h_x0.p, 0, sizeof(R) * C * 8);
     // decay^t table (std::pow, costs.cpp:35)
@@ -1009,6 +1014,7 @@ struct Handle final : HandleBase {
         profile = prof;
         const bool direct = status_direct;
         status_direct = false;
+        graph_direct[which] = direct;
         if (which < 2 && !direct)
           CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
       } catch (...) {
@@ -1048,12 +1054,46 @@ struct Handle final : HandleBase {
     throw Error(code, "device step failed");
   }
 
+  // Wait for a step whose tail publishes the host status itself: spin on the
+  // sequence words (every field is written before them), polling the stream
+  // for errors now and then; false (the caller synchronises the stream) on
+  // an error, a stream that drained without publishing, or after ~2 s.
+  bool wait_published(const std::vector<unsigned long long>& want) {
+    auto seq_ok = [&] {
+      for (int c = 0; c < C; ++c)
+        if (*reinterpret_cast<volatile unsigned long long*>(&h_status.p[c].seq) != want[c]) return false;
+      return true;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long i = 1;; ++i) {
+      if (seq_ok()) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return true;
+      }
+      if ((i & 1023) == 0) {
+        const cudaError_t q = cudaStreamQuery(stream);
+        if (q != cudaErrorNotReady) {
+          if (q == cudaSuccess && seq_ok()) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return true;
+          }
+          return false;
+        }
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) return false;
+      }
+    }
+  }
+
   // mpc_step / compute_control
   void step(const double* x0, double* u0, bool slide) {
     require_ready();
     upload_x0(x0);
-    run_graph(slide ? 0 : 1, slide, false, false);
-    CUDA_TRY(cudaStreamSynchronize(stream));
+    const int which = slide ? 0 : 1;
+    std::vector<unsigned long long>& want = seq_want;
+    want.resize(C);
+    for (int c = 0; c < C; ++c) want[c] = *reinterpret_cast<volatile unsigned long long*>(&h_status.p[c].seq) + 1;
+    run_graph(which, slide, false, false);
+    if (!(graph_direct[which] && wait_published(want))) CUDA_TRY(cudaStreamSynchronize(stream));
     const int code = check_status(true);
     if (code != MPPI_OK) {
       // a failed step leaves plan and iteration untouched (mpc_step throws

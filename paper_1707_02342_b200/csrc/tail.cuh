@@ -55,7 +55,9 @@ __device__ __forceinline__ void tail_prefetch(const EpilogueArgs<float>& a, cons
 // The finished status of controller ctrl into the mapped host mirror (one
 // thread; its own earlier writes to *st are ordered before these reads): the
 // step graph then needs no device-to-host copy node.
-__device__ __forceinline__ void publish_status(const EpilogueArgs<float>& a, int ctrl) {
+// Then the sequence word: seq0 + 1, after a system-scope fence, so a host that
+// sees the new sequence sees every field of this step.
+__device__ __forceinline__ void publish_status(const EpilogueArgs<float>& a, int ctrl, unsigned long long seq0) {
   if (!a.status_host) return;
   const StepStatus* st = a.status + ctrl;
   StepStatus* sh = a.status_host + ctrl;
@@ -65,11 +67,14 @@ __device__ __forceinline__ void publish_status(const EpilogueArgs<float>& a, int
 #pragma unroll
   for (int i = 0; i < 8; ++i) sh->x[i] = st->x[i];
   sh->iteration = st->iteration;
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(&sh->seq) = seq0 + 1;
 }
 
 template <int H>
 __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, const Acc* s_row, int bad, int ctrl,
-                                              unsigned char* smem, const unsigned char* pre, int code0, uint64_t it0) {
+                                              unsigned char* smem, const unsigned char* pre, int code0, uint64_t it0,
+                                              unsigned long long seq0) {
   constexpr int U = H / 32;  // hidden units per lane
   const int T = a.T;
   double* s_agg = reinterpret_cast<double*>(smem);
@@ -97,7 +102,7 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   if (s_code != 0) {
     if (threadIdx.x == 0) {
       if (__ldcg(&st->code) == 0) st->code = s_code;
-      publish_status(a, ctrl);
+      publish_status(a, ctrl, seq0);
     }
     return;
   }
@@ -127,7 +132,7 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   if (__syncthreads_or(nonfinite)) {  // ControlPlan rejects non-finite plans
     if (threadIdx.x == 0) {
       st->code = 1;
-      publish_status(a, ctrl);
+      publish_status(a, ctrl, seq0);
     }
     return;
   }
@@ -201,7 +206,7 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
   if (lane == 0) {
     a.iters[ctrl] = it;
     st->iteration = it;
-    publish_status(a, ctrl);
+    publish_status(a, ctrl, seq0);
   }
 }
 
@@ -232,6 +237,11 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
   // group merge either (a failed step clears the status before the next one)
   const int code0 = (threadIdx.x == 0) ? __ldcg(&ta.e.status[ctrl].code) : 0;
   const uint64_t it0 = ta.e.iters[ctrl];
+  // the host mirror's sequence word (a PCIe read, hidden behind the wait)
+  const unsigned long long seq0 =
+      (threadIdx.x == 0 && ta.e.status_host)
+          ? *reinterpret_cast<const volatile unsigned long long*>(&ta.e.status_host[ctrl].seq)
+          : 0ull;
   cudaGridDependencySynchronize();  // everything below reads the group rows
   if (threadIdx.x == 0) MPPI_STAMP_MIN(3);
   const Acc* P = rows + static_cast<size_t>(ctrl) * ctrl_stride;
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(kTailBlock) tail_kernel(const Acc* __restrict_
   }
   __syncthreads();
   if (threadIdx.x == 0) MPPI_STAMP_MIN(4);  // merged row in shared memory
-  epilogue_fast<H>(ta.e, s_row, bad, ctrl, epi, pre, code0, it0);
+  epilogue_fast<H>(ta.e, s_row, bad, ctrl, epi, pre, code0, it0, seq0);
 #ifdef MPPI_STAMPS
   if (threadIdx.x == 0) {
     volatile unsigned long long* s = g_stamps;
