@@ -232,6 +232,7 @@ struct Handle final : HandleBase {
   int graph_kernels[4] = {0, 0, 0, 0};
   bool graph_direct[4] = {false, false, false, false};  // the graph's tail publishes the host status itself
   bool status_direct = false;      // capture in progress: the tail writes h_status itself
+  bool k1_pdl = false;             // capture in progress: K1 follows the x0 fetch kernel (PDL)
   // sample sharding: NCCL all-gather of the group rows, or (in one process)
   // peer copies from the other handles of a local group
   enum { kExNone = 0, kExNccl = 1, kExLocal = 2 };
@@ -720,6 +721,7 @@ struct Handle final : HandleBase {
     static_assert(sizeof(StepStatus) % sizeof(int) == 0, "StepStatus must be a whole number of ints");
     a.abort_stride = static_cast<int>(sizeof(StepStatus) / sizeof(int));
     a.costs = d_costs.p;
+    a.pdl = k1_pdl && use_tc ? 1 : 0;
     a.partials = d_partials.p;
     return a;
   }
@@ -1003,7 +1005,18 @@ struct Handle final : HandleBase {
         // is clear between steps (throw_status clears it after a failure), so
         // no memset node.  (Reading x0 from the mapped host buffer in K1
         // instead of this copy measured 17 us slower: every warp's PCIe read.)
-        if (which < 2) CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+        // (tensor-core path: a one-CTA fetch kernel instead, K1 its programmatic
+        // dependent, so K1's prologue overlaps the PCIe round trip)
+        k1_pdl = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
+        if (k1_pdl) {
+          if constexpr (std::is_same<R, float>::value) {
+            fetch_x0_kernel<><<<1, 32, 0, stream>>>(h_x0.p, d_x0.p, C * 8);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+          }
+        } else if (which < 2) {
+          CUDA_TRY(cudaMemcpyAsync(d_x0.p, h_x0.p, C * 8 * sizeof(R), cudaMemcpyHostToDevice, stream));
+        }
         const bool prof = profile;
         profile = false;
         n_before_capture = launches;
@@ -1011,6 +1024,7 @@ struct Handle final : HandleBase {
         // mirror itself (no device-to-host copy node at the end of the graph)
         status_direct = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
         enqueue_iteration(cfg.noise_mode, /*events=*/which == 2, slide, /*increment=*/slide, plant, trace);
+        k1_pdl = false;
         profile = prof;
         const bool direct = status_direct;
         status_direct = false;
@@ -1019,6 +1033,7 @@ struct Handle final : HandleBase {
           CUDA_TRY(cudaMemcpyAsync(h_status.p, d_status.p, C * sizeof(StepStatus), cudaMemcpyDeviceToHost, stream));
       } catch (...) {
         status_direct = false;
+        k1_pdl = false;
         cudaStreamEndCapture(stream, &g);
         if (g) cudaGraphDestroy(g);
         throw;

@@ -55,7 +55,17 @@ struct RolloutArgs {
   Acc* partials;          // [C][chunks][partial_stride]
   R* trace_states;        // (T+1) x 7 trajectory of sample trace_k (or nullptr)
   int trace_k;
+  int pdl;                // host: launch K1 as a programmatic dependent (tensor-core path)
 };
+
+// The step graph's first node on the tensor-core path: the controllers'
+// states from the mapped pinned host buffer into device memory (one CTA, a
+// single PCIe round trip), with K1 launched as its programmatic dependent.
+template <int kUnused = 0>
+__global__ void fetch_x0_kernel(const float* __restrict__ host_x0, float* __restrict__ x0, int n) {
+  cudaTriggerProgrammaticLaunchCompletion();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x0[i] = host_x0[i];
+}
 
 template <class R, int Mode>
 __device__ __forceinline__ NoiseStream<R, Mode> make_noise(const RolloutArgs<R>& a, int ctrl, int k) {

@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(32 * NW, tc_min_ctas<H, MT>()) rollout_tc_kern
     v1c = clamp_r(v1, a.sys.lo1, a.sys.hi1);
   };
 
+  cudaGridDependencySynchronize();  // x0 (a no-op unless launched after the x0 fetch)
   const float* x0 = a.x0 + ctrl * 8;
   float px = x0[0], py = x0[1], th = x0[2];
   float roll = x0[3], vx = x0[4], vy = x0[5], thd = x0[6];

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(64 * NP, NP == 1 ? 7 : 4) rollout_tc_pair_kern
   };
 
   // ---- state warp: the 7-state, costmap taps, cost
+  cudaGridDependencySynchronize();  // x0 (a no-op unless launched after the x0 fetch)
   const float* x0 = a.x0 + ctrl * 8;
   float px = x0[0], py = x0[1], th = x0[2];
   float roll = x0[3], vx = x0[4], vy = x0[5], thd = x0[6];

@@ -13,6 +13,25 @@ namespace mppi_host {
 namespace tc_detail {
 constexpr int kTcWarps = 4;  // warps (chunks) per CTA
 
+// K1 launch, as a programmatic dependent of the previous kernel when a.pdl
+// (the step graph's x0 fetch: K1 stages its weights and plan while the state
+// crosses PCIe, and waits for it in cudaGridDependencySynchronize)
+template <class Kern>
+cudaError_t launch_k1(Kern kern, dim3 grid, int threads, size_t smem, cudaStream_t stream,
+                      const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, a, frag);
+}
+
 template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE>
 cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls, size_t smem,
                      cudaStream_t stream) {
@@ -24,8 +43,7 @@ cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
     if (e != cudaSuccess) return e;
   }
   const dim3 grid((n_chunks + kTcWarps - 1) / kTcWarps, ctrls);
-  kern<<<grid, 32 * kTcWarps, smem, stream>>>(a, frag);
-  return cudaGetLastError();
+  return launch_k1(kern, grid, 32 * kTcWarps, smem, stream, a, frag);
 }
 // the per-step state trace (parity: mppi_gpu_rollout_states) is its own instantiation
 template <int H, int MT, int Mode, bool STAB, bool STORE>
@@ -70,8 +88,7 @@ cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
   if (e != cudaSuccess) return e;
   const dim3 grid((n_chunks + kTcPairs - 1) / kTcPairs, ctrls);
   g_tc_last_pair = 1;
-  kern<<<grid, 64 * kTcPairs, smem, stream>>>(a, frag);
-  return cudaGetLastError();
+  return launch_k1(kern, grid, 64 * kTcPairs, smem, stream, a, frag);
 }
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (tc_min_ctas CTAs of 4 warps per SM); larger launches regenerate it from
