@@ -1007,6 +1007,7 @@ struct Handle final : HandleBase {
         // instead of this copy measured 17 us slower: every warp's PCIe read.)
         // (tensor-core path: a one-CTA fetch kernel instead, K1 its programmatic
         // dependent, so K1's prologue overlaps the PCIe round trip)
+        n_before_capture = launches;
         k1_pdl = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
         if (k1_pdl) {
           if constexpr (std::is_same<R, float>::value) {
@@ -1019,7 +1020,6 @@ struct Handle final : HandleBase {
         }
         const bool prof = profile;
         profile = false;
-        n_before_capture = launches;
         // step graphs on the tensor-core path: the tail writes the host status
         // mirror itself (no device-to-host copy node at the end of the graph)
         status_direct = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
