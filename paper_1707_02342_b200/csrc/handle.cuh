@@ -24,6 +24,7 @@
 #include "epilogue.cuh"
 #include "group.cuh"
 #include "rollout_tc.cuh"
+#include "rollout_umma.cuh"
 #include "cem.cuh"
 #include "ws_launch.hpp"
 #include "errors.hpp"
@@ -162,6 +163,65 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
   }
   return f;
 }
+// The weight image of the tcgen05 rollout (rollout_umma.cuh, UmmaLayout): the
+// same folded weights as tc_build_fragments (layer 3 on 2^s-scaled weights),
+// as fp16 hi / lo B tiles in the canonical K-major layout, plus the layer-2/3
+// bias vectors (added after the accumulator read-back) and 2^-s.
+template <class R>
+std::vector<unsigned char> umma_build_image(const MlpParams<R, 32>& w) {
+  using U = mppi_dev::UmmaLayout;
+  constexpr int H = 32;
+  const double kk2 = 2.0 / std::log(2.0);
+  auto W1 = [&](int n, int i) { return static_cast<double>(w.w1t[i][n]); };
+  auto W2 = [&](int n, int i) { return static_cast<double>(w.w2t[i][n]); };
+  auto W3 = [&](int n, int i) { return static_cast<double>(w.w3t[i][n]); };
+  double w3max = 0.0;
+  for (int n = 0; n < 4; ++n)
+    for (int i = 0; i < H; ++i) w3max = std::max(w3max, std::abs(2.0 * W3(n, i)));
+  int s3 = 0;
+  while (s3 < 12 && w3max > 0.0 && w3max * std::ldexp(1.0, s3 + 1) < 1.0) ++s3;
+  if (const char* e = std::getenv("MPPI_TC_W3_SHIFT")) s3 = std::max(0, std::min(12, std::atoi(e)));
+  const double sc3 = std::ldexp(1.0, s3);
+  std::vector<unsigned char> img(U::BYTES, 0);
+  auto put_half = [&](uint32_t base, int row, int k, double v, bool lo) {
+    const __half h = __double2half(v);
+    const __half x = lo ? __double2half(v - static_cast<double>(__half2float(h))) : h;
+    const uint16_t bits = __half_as_ushort(x);
+    std::memcpy(&img[base + mppi_dev::umma_tile_offset(row, k)], &bits, 2);
+  };
+  for (int lo = 0; lo < 2; ++lo) {
+    for (int n = 0; n < H; ++n)
+      for (int k = 0; k < 16; ++k) {
+        const double v = k < 6 ? kk2 * W1(n, k) : (k == 6 ? kk2 * static_cast<double>(w.b1[n]) : 0.0);
+        put_half(lo ? U::W1_LO : U::W1_HI, n, k, v, lo != 0);
+      }
+    for (int s = 0; s < 2; ++s)
+      for (int n = 0; n < H; ++n)
+        for (int k = 0; k < 16; ++k)
+          put_half((lo ? U::W2_LO : U::W2_HI) + 1024 * s, n, k, 2.0 * kk2 * W2(n, 16 * s + k), lo != 0);
+    for (int s = 0; s < 2; ++s)
+      for (int n = 0; n < 16; ++n)
+        for (int k = 0; k < 16; ++k)
+          put_half((lo ? U::W3_LO : U::W3_HI) + 512 * s, n, k, n < 4 ? sc3 * 2.0 * W3(n, 16 * s + k) : 0.0,
+                   lo != 0);
+  }
+  for (int n = 0; n < H; ++n) {
+    double sum = 0.0;
+    for (int i = 0; i < H; ++i) sum += W2(n, i);
+    const float v = static_cast<float>(kk2 * (static_cast<double>(w.b2[n]) + sum));
+    std::memcpy(&img[U::B2 + 4 * n], &v, 4);
+  }
+  for (int o = 0; o < 4; ++o) {
+    double sum = 0.0;
+    for (int i = 0; i < H; ++i) sum += W3(o, i);
+    const float v = static_cast<float>(sc3 * (static_cast<double>(w.b3[o]) + sum));
+    std::memcpy(&img[U::B3 + 4 * o], &v, 4);
+  }
+  const float inv = static_cast<float>(std::ldexp(1.0, -s3));
+  std::memcpy(&img[U::SC], &inv, 4);
+  return img;
+}
+
 constexpr int kEpiBlock = 512;   // K2 CTA
 
 template <class R>
@@ -189,7 +249,10 @@ struct Handle final : HandleBase {
   }
   std::string variant_name() const override {
     char buf[160];
-    if (use_tc && tc_pair_used == 1)
+    if (use_umma)
+      std::snprintf(buf, sizeof(buf), "rollout_umma_kernel<f32,H=32,noise=%d> (tcgen05.mma f16x3 M=128, TMEM accumulators, chunk 128, %d chunks, %d groups, group merge + tail kernels)",
+                    cfg.noise_mode, n_chunks, n_groups);
+    else if (use_tc && tc_pair_used == 1)
       std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);
     else if (use_tc)
@@ -224,6 +287,8 @@ struct Handle final : HandleBase {
   bool ws_smem_w = true;  // weights staged in shared memory (vs constant bank)
   // tensor-core K1 (rollout_tc.cuh): fp32 vehicle model, H = 32; chunk = 16*tc_mt
   bool use_tc = false;
+  bool use_umma = false;  // K1 on tcgen05 / TMEM (rollout_umma.cuh), H = 32; the tensor-core tail as use_tc
+  DevBuf<unsigned char> d_umma;
   int tc_mt = 2;
   int tc_pair_used = -1;  // whether this handle's last K1 launch was the warp-pair kernel (-1: none yet)
   DevBuf<uint32_t> d_tcfrag;
@@ -387,6 +452,16 @@ struct Handle final : HandleBase {
     // default K1 for the fp32 vehicle model: tensor cores at H = 32, FFMA2
     // warp-specialised at H = 64 (its weights do not fit the register file)
     use_tc = f32_vehicle && !force_generic && kernel != "ws";
+    // H = 32 from 65 536 samples on (counting every controller of a fleet):
+    // K1 on tcgen05 / TMEM, one sample per thread (rollout_umma.cuh; measured
+    // 4-8 % faster than the mma.sync kernel there, profiles/README.md);
+    // MPPI_KERNEL=umma forces it, MPPI_KERNEL=mma keeps the mma.sync kernel
+    const bool umma_default = static_cast<long long>(K) * C >= 65536;
+    if (use_tc && H == 32 && (kernel == "umma" || (umma_default && kernel != "mma"))) {
+      use_umma = true;
+      chunk_samples = mppi_dev::kUmmaThreads;
+      return;
+    }
     if (use_tc) {
       // one m16 tile per warp while warps are scarce (counting every
       // controller of a fleet), two once the grid fills the GPU several times
@@ -500,6 +575,13 @@ struct Handle final : HandleBase {
       if (!std::isfinite(w1[i])) throw_invalid("MLP weights must be finite");
     auto upload_tc = [&](const auto& w) {
       if (!use_tc) return;
+      if constexpr (std::is_same<std::decay_t<decltype(w)>, MlpParams<R, 32>>::value) {
+        if (use_umma) {
+          const std::vector<unsigned char> img = umma_build_image(w);
+          d_umma.alloc(img.size());
+          CUDA_TRY(cudaMemcpy(d_umma.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+        }
+      }
       std::vector<uint32_t> frag = tc_build_fragments(w);
       d_tcfrag.alloc(frag.size());
       CUDA_TRY(cudaMemcpy(d_tcfrag.p, frag.data(), frag.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -811,7 +893,10 @@ struct Handle final : HandleBase {
     // it is marked external; external records become graph event nodes
     if (events) CUDA_TRY(cudaEventRecordWithFlags(ev_a, stream, cudaEventRecordExternal));
     else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
-    if (use_tc) {
+    if (use_umma) {
+      if constexpr (std::is_same<R, float>::value)
+        CUDA_TRY(launch_rollout_umma(a, d_umma.p, mode, chunk_hi - chunk_lo, C, stream));
+    } else if (use_tc) {
       if constexpr (std::is_same<R, float>::value)
         CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, mode, tc_mt,
                                                                           chunk_hi - chunk_lo, C, stream));
@@ -1368,7 +1453,10 @@ struct Handle final : HandleBase {
       a.chunk0 = 0;
       a.chunk_end = n_chunks;
       CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
-      if (use_tc) {
+      if (use_umma) {
+        if constexpr (std::is_same<R, float>::value)
+          CUDA_TRY(launch_rollout_umma(a, d_umma.p, effective_mode(batch_injected), n_chunks, 1, stream));
+      } else if (use_tc) {
         if constexpr (std::is_same<R, float>::value)
           CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, effective_mode(batch_injected),
                                                                             tc_mt, n_chunks, 1, stream));

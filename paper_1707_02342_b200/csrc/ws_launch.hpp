@@ -42,6 +42,10 @@ extern template cudaError_t launch_tail_tc<32>(const mppi_dev::Acc*, int, int, l
                                                const mppi_dev::TailArgs&, int, bool, cudaStream_t);
 extern template cudaError_t launch_tail_tc<64>(const mppi_dev::Acc*, int, int, long long, double,
                                                const mppi_dev::TailArgs&, int, bool, cudaStream_t);
+// The tcgen05 / TMEM rollout (rollout_umma.cuh), H = 32: chunks of 128
+// samples from a.chunk0; wimg is the weight image (umma_build_image).
+cudaError_t launch_rollout_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned char* wimg, int mode,
+                                int n_chunks, int ctrls, cudaStream_t stream);
 // Fixed-group merge of the chunk partials (group.cuh): groups [g0, g0 + n_local)
 // of n_groups; programmatic dependent of the previous kernel when pdl.
 cudaError_t launch_group_merge(const mppi_dev::Acc* partials, long long partials_ctrl_stride, int n_chunks,
