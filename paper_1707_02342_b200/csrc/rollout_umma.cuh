@@ -86,9 +86,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   uint32_t done = 0;
   do {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
-        : "r"(mbar), "r"(phase)
+        : "r"(mbar), "r"(phase), "r"(0x989680u)  // suspend-time hint: sleep until the phase completes
         : "memory");
   } while (!done);
 }
