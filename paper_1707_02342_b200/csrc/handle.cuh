@@ -449,8 +449,9 @@ struct Handle final : HandleBase {
     const std::string kernel = kv ? kv : "";
     const bool force_generic = kernel == "generic";
     const bool f32_vehicle = std::is_same<R, float>::value && cfg.system == MPPI_SYSTEM_VEHICLE_MLP;
-    // default K1 for the fp32 vehicle model: tensor cores at H = 32, FFMA2
-    // warp-specialised at H = 64 (its weights do not fit the register file)
+    // default K1 for the fp32 vehicle model: tensor cores at H = 32 and 64
+    // (MPPI_KERNEL=ws: the FFMA2 warp-specialised kernel, generic: one thread
+    // per sample)
     use_tc = f32_vehicle && !force_generic && kernel != "ws";
     // H = 32 from 65 536 samples on (counting every controller of a fleet):
     // K1 on tcgen05 / TMEM, one sample per thread (rollout_umma.cuh; measured
