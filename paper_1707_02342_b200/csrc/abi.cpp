@@ -2,6 +2,7 @@
 // converts exceptions to MPPI_* status codes (mppi_gpu_last_error() holds the
 // message) and forwards to the precision-specific handle.
 #include <cuda_runtime_api.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstring>
@@ -13,6 +14,7 @@
 #include "nccl_api.hpp"
 #include "shard.hpp"
 
+#include <utility>
 #include <vector>
 
 using namespace mppi_host;
@@ -26,6 +28,22 @@ int with_handle(mppi_gpu_handle* h, F&& f) {
     CUDA_TRY(cudaSetDevice(h->impl->device_index()));
     f(*h->impl);
   });
+}
+
+// NVTX3 range around a hot-path entry point (SURVEY §5 tracing plan): the
+// iteration itself is one graph replay, so the range brackets its launch and
+// host-side wait; nsys / ncu --nvtx attribute the kernels to it.  A branch on
+// a null pointer when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+template <class F>
+int with_handle_traced(const char* name, mppi_gpu_handle* h, F&& f) {
+  NvtxRange r(name);
+  return with_handle(h, std::forward<F>(f));
 }
 
 }  // namespace
@@ -175,7 +193,7 @@ int mppi_gpu_set_noise(mppi_gpu_handle* h, const double* eps) {
   });
 }
 int mppi_gpu_compute_control(mppi_gpu_handle* h, const double* x0, double* u0_out) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_compute_control", h, [&](auto& x) {
     if (!x0) throw_invalid("compute_control: null x0");
     x.step(x0, u0_out, false);
   });
@@ -184,27 +202,27 @@ int mppi_gpu_slide(mppi_gpu_handle* h) {
   return with_handle(h, [&](auto& x) { x.slide_only(); });
 }
 int mppi_gpu_step(mppi_gpu_handle* h, const double* x0, double* u0_out) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_step", h, [&](auto& x) {
     if (!x0) throw_invalid("step: null x0");
     x.step(x0, u0_out, true);
   });
 }
 int mppi_gpu_optimize(mppi_gpu_handle* h, const double* x0, int iterations) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_optimize", h, [&](auto& x) {
     if (!x0) throw_invalid("optimize: null x0");
     x.optimize(x0, iterations);
   });
 }
 int mppi_gpu_closed_loop(mppi_gpu_handle* h, const double* x_init, int iterations, double* u_trace,
                          double* x_trace) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_closed_loop", h, [&](auto& x) {
     if (!x_init) throw_invalid("closed_loop: null x_init");
     x.closed_loop(x_init, iterations, u_trace, x_trace, 0, nullptr, nullptr);
   });
 }
 int mppi_gpu_closed_loop_timed(mppi_gpu_handle* h, const double* x_init, int iterations,
                                uint64_t flush_l2_bytes, double* device_ms_out, double* iter_ms_out) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_closed_loop_timed", h, [&](auto& x) {
     if (!x_init) throw_invalid("closed_loop: null x_init");
     if (iter_ms_out && flush_l2_bytes == 0) throw_invalid("closed_loop_timed: per-iteration times need flush mode");
     x.closed_loop(x_init, iterations, nullptr, nullptr, static_cast<size_t>(flush_l2_bytes), device_ms_out,
@@ -220,20 +238,20 @@ int mppi_gpu_sample_perturbations(mppi_gpu_handle* h, uint64_t iteration, double
 }
 int mppi_gpu_rollout_costs(mppi_gpu_handle* h, const double* x0, const double* eps_in,
                            double* costs_out, double* eps_stored_out) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_rollout_costs", h, [&](auto& x) {
     if (!x0 || !costs_out) throw_invalid("rollout_costs: null");
     if (x.controllers() != 1) throw Error(MPPI_ERR_UNSUPPORTED, "parity entry points use single-controller handles");
     x.rollout_costs(x0, eps_in, costs_out, eps_stored_out);
   });
 }
 int mppi_gpu_weights(mppi_gpu_handle* h, const double* costs, double* w_out, double* rho, double* eta) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_weights", h, [&](auto& x) {
     if (!costs || !w_out || !rho || !eta) throw_invalid("weights: null");
     x.weights(costs, w_out, rho, eta);
   });
 }
 int mppi_gpu_update_plan(mppi_gpu_handle* h, const double* weights) {
-  return with_handle(h, [&](auto& x) {
+  return with_handle_traced("mppi_gpu_update_plan", h, [&](auto& x) {
     if (!weights) throw_invalid("update_plan: null");
     x.update_plan(weights);
   });
@@ -276,6 +294,7 @@ int mppi_gpu_set_comm_local(mppi_gpu_handle** handles, int n) {
 }
 int mppi_gpu_step_local(mppi_gpu_handle** handles, int n, const double* x0, double* u0_out) {
   return guard([&] {
+    NvtxRange range("mppi_gpu_step_local");
     if (!handles || n < 1 || !x0) throw_invalid("step_local: null argument");
     for (int i = 0; i < n; ++i)
       if (!handles[i] || !handles[i]->impl) throw_invalid("step_local: null handle");

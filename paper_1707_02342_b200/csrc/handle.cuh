@@ -167,10 +167,9 @@ std::vector<uint32_t> tc_build_fragments(const MlpParams<R, H>& w) {
 // same folded weights as tc_build_fragments (layer 3 on 2^s-scaled weights),
 // as fp16 hi / lo B tiles in the canonical K-major layout, plus the layer-2/3
 // bias vectors (added after the accumulator read-back) and 2^-s.
-template <class R>
-std::vector<unsigned char> umma_build_image(const MlpParams<R, 32>& w) {
-  using U = mppi_dev::UmmaLayout;
-  constexpr int H = 32;
+template <class R, int H>
+std::vector<unsigned char> umma_build_image(const MlpParams<R, H>& w) {
+  using U = mppi_dev::UmmaLayout<H>;
   const double kk2 = 2.0 / std::log(2.0);
   auto W1 = [&](int n, int i) { return static_cast<double>(w.w1t[i][n]); };
   auto W2 = [&](int n, int i) { return static_cast<double>(w.w2t[i][n]); };
@@ -195,11 +194,11 @@ std::vector<unsigned char> umma_build_image(const MlpParams<R, 32>& w) {
         const double v = k < 6 ? kk2 * W1(n, k) : (k == 6 ? kk2 * static_cast<double>(w.b1[n]) : 0.0);
         put_half(lo ? U::W1_LO : U::W1_HI, n, k, v, lo != 0);
       }
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < U::NK; ++s)
       for (int n = 0; n < H; ++n)
         for (int k = 0; k < 16; ++k)
-          put_half((lo ? U::W2_LO : U::W2_HI) + 1024 * s, n, k, 2.0 * kk2 * W2(n, 16 * s + k), lo != 0);
-    for (int s = 0; s < 2; ++s)
+          put_half((lo ? U::W2_LO : U::W2_HI) + 32 * H * s, n, k, 2.0 * kk2 * W2(n, 16 * s + k), lo != 0);
+    for (int s = 0; s < U::NK; ++s)
       for (int n = 0; n < 16; ++n)
         for (int k = 0; k < 16; ++k)
           put_half((lo ? U::W3_LO : U::W3_HI) + 512 * s, n, k, n < 4 ? sc3 * 2.0 * W3(n, 16 * s + k) : 0.0,
@@ -250,8 +249,8 @@ struct Handle final : HandleBase {
   std::string variant_name() const override {
     char buf[160];
     if (use_umma)
-      std::snprintf(buf, sizeof(buf), "rollout_umma_kernel<f32,H=32,noise=%d> (tcgen05.mma f16x3 M=128, TMEM accumulators, chunk 128, %d chunks, %d groups, group merge + tail kernels)",
-                    cfg.noise_mode, n_chunks, n_groups);
+      std::snprintf(buf, sizeof(buf), "rollout_umma_kernel<f32,H=%d,noise=%d> (tcgen05.mma f16x3 M=128, TMEM accumulators, chunk 128, %d chunks, %d groups, group merge + tail kernels)",
+                    H, cfg.noise_mode, n_chunks, n_groups);
     else if (use_tc && tc_pair_used == 1)
       std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);
@@ -287,7 +286,7 @@ struct Handle final : HandleBase {
   bool ws_smem_w = true;  // weights staged in shared memory (vs constant bank)
   // tensor-core K1 (rollout_tc.cuh): fp32 vehicle model, H = 32; chunk = 16*tc_mt
   bool use_tc = false;
-  bool use_umma = false;  // K1 on tcgen05 / TMEM (rollout_umma.cuh), H = 32; the tensor-core tail as use_tc
+  bool use_umma = false;  // K1 on tcgen05 / TMEM (rollout_umma.cuh); the tensor-core tail as use_tc
   DevBuf<unsigned char> d_umma;
   int tc_mt = 2;
   int tc_pair_used = -1;  // whether this handle's last K1 launch was the warp-pair kernel (-1: none yet)
@@ -453,12 +452,14 @@ struct Handle final : HandleBase {
     // (MPPI_KERNEL=ws: the FFMA2 warp-specialised kernel, generic: one thread
     // per sample)
     use_tc = f32_vehicle && !force_generic && kernel != "ws";
-    // H = 32 from 65 536 samples on (counting every controller of a fleet):
-    // K1 on tcgen05 / TMEM, one sample per thread (rollout_umma.cuh; measured
-    // 4-8 % faster than the mma.sync kernel there, profiles/README.md);
-    // MPPI_KERNEL=umma forces it, MPPI_KERNEL=mma keeps the mma.sync kernel
-    const bool umma_default = static_cast<long long>(K) * C >= 65536;
-    if (use_tc && H == 32 && (kernel == "umma" || (umma_default && kernel != "mma"))) {
+    // From 32 768 samples on (counting every controller of a fleet): K1 on
+    // tcgen05 / TMEM, one sample per thread (rollout_umma.cuh; measured at
+    // H = 32 3-10 % faster than the mma.sync kernel there and 1.8x slower at
+    // 16 384, where it runs one 4-warp CTA per SM; at H = 64 (c2) 11 %
+    // faster; profiles/README.md).  MPPI_KERNEL=umma forces it,
+    // MPPI_KERNEL=mma keeps the mma.sync kernel
+    const bool umma_default = static_cast<long long>(K) * C >= 32768;
+    if (use_tc && (kernel == "umma" || (umma_default && kernel != "mma"))) {
       use_umma = true;
       chunk_samples = mppi_dev::kUmmaThreads;
       return;
@@ -576,12 +577,10 @@ struct Handle final : HandleBase {
       if (!std::isfinite(w1[i])) throw_invalid("MLP weights must be finite");
     auto upload_tc = [&](const auto& w) {
       if (!use_tc) return;
-      if constexpr (std::is_same<std::decay_t<decltype(w)>, MlpParams<R, 32>>::value) {
-        if (use_umma) {
-          const std::vector<unsigned char> img = umma_build_image(w);
-          d_umma.alloc(img.size());
-          CUDA_TRY(cudaMemcpy(d_umma.p, img.data(), img.size(), cudaMemcpyHostToDevice));
-        }
+      if (use_umma) {
+        const std::vector<unsigned char> img = umma_build_image(w);
+        d_umma.alloc(img.size());
+        CUDA_TRY(cudaMemcpy(d_umma.p, img.data(), img.size(), cudaMemcpyHostToDevice));
       }
       std::vector<uint32_t> frag = tc_build_fragments(w);
       d_tcfrag.alloc(frag.size());
@@ -896,7 +895,8 @@ struct Handle final : HandleBase {
     else if (profile) CUDA_TRY(cudaEventRecord(ev_a, stream));
     if (use_umma) {
       if constexpr (std::is_same<R, float>::value)
-        CUDA_TRY(launch_rollout_umma(a, d_umma.p, mode, chunk_hi - chunk_lo, C, stream));
+        CUDA_TRY((H == 32 ? launch_rollout_umma<32> : launch_rollout_umma<64>)(a, d_umma.p, mode, chunk_hi - chunk_lo,
+                                                                              C, stream));
     } else if (use_tc) {
       if constexpr (std::is_same<R, float>::value)
         CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, mode, tc_mt,
@@ -1456,7 +1456,8 @@ struct Handle final : HandleBase {
       CUDA_TRY(cudaMemcpyAsync(d_states.p, h_x0.p, 7 * sizeof(R), cudaMemcpyHostToDevice, stream));
       if (use_umma) {
         if constexpr (std::is_same<R, float>::value)
-          CUDA_TRY(launch_rollout_umma(a, d_umma.p, effective_mode(batch_injected), n_chunks, 1, stream));
+          CUDA_TRY((H == 32 ? launch_rollout_umma<32> : launch_rollout_umma<64>)(
+              a, d_umma.p, effective_mode(batch_injected), n_chunks, 1, stream));
       } else if (use_tc) {
         if constexpr (std::is_same<R, float>::value)
           CUDA_TRY((H == 32 ? launch_rollout_tc<32> : launch_rollout_tc<64>)(a, d_tcfrag.p, effective_mode(batch_injected),

@@ -1,5 +1,5 @@
 // rollout_umma.cuh — K1 on the 5th-generation tensor cores (tcgen05 / TMEM),
-// H = 32, for the throughput configurations.
+// H = 32 and 64, for the throughput configurations.
 //
 // One CTA of 128 threads owns a chunk of 128 samples, ONE SAMPLE PER THREAD:
 // thread r runs sample r's whole scalar path (Philox noise, coupling, clamp,
@@ -7,12 +7,12 @@
 // per-layer M = 128 tile.  Per step and layer the threads stage their rows
 // of the A operand (fp16 hi and lo of the layer input) in shared memory in
 // the canonical K-major no-swizzle UMMA layout, one elected thread issues the
-// layer's tcgen05.mma (M = 128, N = 32 or 16, K = 16; hi*hi into one TMEM
+// layer's tcgen05.mma (M = 128, N = H or 16, K = 16 per slice; hi*hi into one TMEM
 // accumulator, hi*lo + lo*hi into another, as the mma.sync kernel's m/c
 // split), commits them to an mbarrier, and every thread reads its row back
 // with tcgen05.ld (TMEM lane = thread).  Weights (B operands, fp16 hi/lo,
 // tanh folded as in rollout_tc.cuh) stay in shared memory for the whole
-// rollout; the accumulators use 64 TMEM columns per CTA.
+// rollout; the accumulators use 2H TMEM columns per CTA.
 //
 // Compared with the mma.sync kernel this removes the warp-issued HMMAs, the
 // fragment bookkeeping and the mirror-lane duplication of the scalar path; it
@@ -29,15 +29,29 @@
 namespace mppi_dev {
 
 constexpr int kUmmaThreads = 128;  // samples (= TMEM lanes, = MMA M) per CTA
-// bit p: pair p of every 8 activations takes the FMA-pipe reciprocal (the rest the SFU)
-#ifndef MPPI_UMMA_SW
-#define MPPI_UMMA_SW 10
+// bit p: pair p of every 8 activations takes the FMA-pipe reciprocal (the rest
+// the SFU); H = 64 defaults to the SFU for all of them, as the mma.sync kernel
+template <int H>
+__host__ __device__ constexpr int umma_sw_rcp() {
+#ifdef MPPI_UMMA_SW
+  return MPPI_UMMA_SW;
+#else
+  return H == 32 ? 10 : 0;
 #endif
-constexpr int kUmmaSwRcp = MPPI_UMMA_SW;
-#ifndef MPPI_UMMA_CTAS
-#define MPPI_UMMA_CTAS 4
+}
+// resident CTAs per SM the register budget is sized for (H = 64: three, the
+// shared-memory footprint allows no more)
+template <int H>
+__host__ __device__ constexpr int umma_min_ctas() {
+#ifdef MPPI_UMMA_CTAS
+  return MPPI_UMMA_CTAS;
+#else
+  return H == 32 ? 4 : 3;
 #endif
-constexpr int kUmmaTmemCols = 64;  // accumulators: [0, 32) hi*hi, [32, 64) cross terms
+}
+// accumulators: [0, H) hi*hi, [H, 2H) cross terms
+template <int H>
+__host__ __device__ constexpr int umma_tmem_cols() { return 2 * H; }
 
 // Byte offset of element (row, k) of a K = 16 fp16 tile in the canonical
 // K-major, no-swizzle layout: 8-row x 16-byte core matrices, the two K halves
@@ -47,14 +61,17 @@ __host__ __device__ constexpr uint32_t umma_tile_offset(int row, int k) {
 }
 constexpr uint32_t kUmmaTileA = 128 * 32;  // bytes of an M = 128, K = 16 fp16 tile
 // Weight image (host-built, copied to shared memory as is): fp16 B tiles in
-// the layout above, then the fp32 bias vectors and the layer-3 scale.
+// the layout above (N rows x K = 16 per slice; layers 2/3 have H/16 K slices),
+// then the fp32 bias vectors and the layer-3 scale.
+template <int H>
 struct UmmaLayout {
-  static constexpr uint32_t W1_HI = 0, W1_LO = 1024;                       // N = 32, K = 16
-  static constexpr uint32_t W2_HI = 2048, W2_LO = W2_HI + 2048;            // 2 K slices x 1 KB
-  static constexpr uint32_t W3_HI = W2_LO + 2048, W3_LO = W3_HI + 1024;    // N = 16: 2 K slices x 512 B
-  static constexpr uint32_t B2 = W3_LO + 1024;                             // 32 floats
-  static constexpr uint32_t B3 = B2 + 128;                                 // 4 floats (+ pad)
-  static constexpr uint32_t SC = B3 + 16;                                  // 2^-s (1 float)
+  static constexpr int NK = H / 16;                                         // K slices of layers 2 and 3
+  static constexpr uint32_t W1_HI = 0, W1_LO = 32 * H;                      // N = H, K = 16
+  static constexpr uint32_t W2_HI = 64 * H, W2_LO = W2_HI + NK * 32 * H;    // NK slices x (32 H) B
+  static constexpr uint32_t W3_HI = W2_LO + NK * 32 * H, W3_LO = W3_HI + NK * 512;  // N = 16: NK x 512 B
+  static constexpr uint32_t B2 = W3_LO + NK * 512;                          // H floats
+  static constexpr uint32_t B3 = B2 + 4 * H;                                // 4 floats (+ pad)
+  static constexpr uint32_t SC = B3 + 16;                                   // 2^-s (1 float)
   static constexpr uint32_t BYTES = ((SC + 4) + 15) & ~15u;
 };
 
@@ -96,20 +113,7 @@ __device__ __forceinline__ void tc05_before_sync() { asm volatile("tcgen05.fence
 __device__ __forceinline__ void tc05_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void proxy_fence_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// 32 / 16 consecutive fp32 TMEM columns of this thread's lane.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
+// 16 / 4 consecutive fp32 TMEM columns of this thread's lane.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -137,41 +141,66 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-// Activations of one 32-wide hidden layer (tanh folded: s = -1/(1 + 2^y),
-// pairs alternately on the SFU and the FMA-pipe reciprocal) into this
-// thread's rows of the next layer's A tiles (two K slices, hi and lo planes).
-__device__ __forceinline__ void umma_stage_act(const float (&y)[32], uint32_t a_hi, uint32_t a_lo, int row) {
+// One hidden layer from TMEM to the next layer's A operand, two K slices
+// (32 hidden units) at a time: this thread's row of the hi*hi and cross
+// accumulators of both slices first (one tcgen05.wait), then per unit the sum
+// (+ the bias when BIAS), the activation (tanh folded: s = -1/(1 + 2^y), pairs on the
+// SFU or the FMA-pipe reciprocal per SW), the fp16 hi/lo split, and the rows
+// of the A tiles (hi and lo planes) — the 16 activation pairs of a group are
+// independent chains the scheduler interleaves.
+template <int H, int SW, bool BIAS>
+__device__ __forceinline__ void umma_layer_to_a(uint32_t t_lane, const float* __restrict__ bias, uint32_t a_hi,
+                                                uint32_t a_lo, int row) {
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
+  for (int s0 = 0; s0 < H / 16; s0 += 2) {
+    float y[32];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // K halves of slice s: hidden 16s + 8h .. +7
-      uint32_t hw[4], lw[4];
+    for (int q = 0; q < 2; ++q) {
+      float m16[16], c16[16];
+      tmem_ld16(t_lane + 16 * (s0 + q), m16);
+      tmem_ld16(t_lane + H + 16 * (s0 + q), c16);
+      tmem_wait_ld();
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int j = 16 * s + 8 * h + 2 * p;
-        const float2 r = ((kUmmaSwRcp >> p) & 1) ? act_r2<true>(y[j], y[j + 1]) : act_r2<false>(y[j], y[j + 1]);
-        split2(r.x, r.y, hw[p], lw[p]);
+      for (int j = 0; j < 16; j += 2) {
+        float2 z = __fadd2_rn(make_float2(m16[j], m16[j + 1]), make_float2(c16[j], c16[j + 1]));
+        if constexpr (BIAS) z = __fadd2_rn(z, make_float2(bias[16 * (s0 + q) + j], bias[16 * (s0 + q) + j + 1]));
+        y[16 * q + j] = z.x;
+        y[16 * q + j + 1] = z.y;
       }
-      const uint32_t off = static_cast<uint32_t>(s) * kUmmaTileA + umma_tile_offset(row, 8 * h);
-      sts128(a_hi + off, hw[0], hw[1], hw[2], hw[3]);
-      sts128(a_lo + off, lw[0], lw[1], lw[2], lw[3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // K halves of slice s0 + q: hidden 16 (s0 + q) + 8h .. +7
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int j = 16 * q + 8 * h + 2 * p;
+          const float2 r = ((SW >> p) & 1) ? act_r2<true>(y[j], y[j + 1]) : act_r2<false>(y[j], y[j + 1]);
+          split2(r.x, r.y, hw[p], lw[p]);
+        }
+        const uint32_t off = static_cast<uint32_t>(s0 + q) * kUmmaTileA + umma_tile_offset(row, 8 * h);
+        sts128(a_hi + off, hw[0], hw[1], hw[2], hw[3]);
+        sts128(a_lo + off, lw[0], lw[1], lw[2], lw[3]);
+      }
     }
   }
 }
 
 // grid = (chunks of 128 samples, controllers), block = 128.  Dynamic smem:
-// plan (2T + 2 floats) | weight image (UmmaLayout) | A tiles: layer 1 hi/lo
-// (2 x 4 KB), layers 2/3 hi/lo x 2 K slices (4 x 4 KB) | numerator staging
+// plan (2T + 2 floats) | weight image (UmmaLayout<H>) | A tiles: layer 1 hi/lo
+// (2 x 4 KB), layers 2/3 hi/lo x H/16 K slices | numerator staging
 // (kTcTB x 2 x 128 doubles, aliased on the A tiles after the rollout).
+template <int H>
 __host__ __device__ constexpr size_t umma_smem_bytes(int T) {
   const size_t plan = (sizeof(float) * (2 * T + 2) + 127) & ~size_t(127);
-  const size_t tiles = 6 * kUmmaTileA;
+  const size_t tiles = (2 + 2 * (H / 16)) * kUmmaTileA;
   const size_t stage = sizeof(double) * kTcTB * 2 * kUmmaThreads;
-  return plan + UmmaLayout::BYTES + (tiles > stage ? tiles : stage) + 128;
+  return plan + UmmaLayout<H>::BYTES + (tiles > stage ? tiles : stage) + 128;
 }
 
-template <int Mode, bool STAB, bool TRACE>
-__global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_kernel(const __grid_constant__ RolloutArgs<float> a,
+template <int H, int Mode, bool STAB, bool TRACE>
+__global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                                        const unsigned char* __restrict__ wimg) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_taddr;
@@ -190,13 +219,16 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
 
   float* s_plan = reinterpret_cast<float*>(smem_raw);
   unsigned char* s_w = smem_raw + ((sizeof(float) * (2 * T + 2) + 127) & ~size_t(127));
-  unsigned char* s_tiles = s_w + UmmaLayout::BYTES;
+  using UL = UmmaLayout<H>;
+  constexpr int NK = UL::NK;
+  constexpr int SW = umma_sw_rcp<H>();
+  unsigned char* s_tiles = s_w + UL::BYTES;
   s_tiles = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_tiles) + 127) & ~uintptr_t(127));
   const uint32_t w_addr = static_cast<uint32_t>(__cvta_generic_to_shared(s_w));
   const uint32_t a1_hi = static_cast<uint32_t>(__cvta_generic_to_shared(s_tiles));
   const uint32_t a1_lo = a1_hi + kUmmaTileA;
-  const uint32_t a2_hi = a1_lo + kUmmaTileA;       // 2 K slices
-  const uint32_t a2_lo = a2_hi + 2 * kUmmaTileA;   // 2 K slices
+  const uint32_t a2_hi = a1_lo + kUmmaTileA;        // NK K slices
+  const uint32_t a2_lo = a2_hi + NK * kUmmaTileA;   // NK K slices
   const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
 
   for (int i = tid; i < 2 * T + 2; i += kUmmaThreads)
@@ -204,7 +236,7 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
   {
     const uint4* src = reinterpret_cast<const uint4*>(wimg);
     uint4* dst = reinterpret_cast<uint4*>(s_w);
-    for (int i = tid; i < static_cast<int>(UmmaLayout::BYTES / 16); i += kUmmaThreads) dst[i] = src[i];
+    for (int i = tid; i < static_cast<int>(UL::BYTES / 16); i += kUmmaThreads) dst[i] = src[i];
   }
   // the constant-one input (k = 6, the layer-1 bias column) and the zero K
   // half (k = 8 .. 15) of this thread's layer-1 rows, written once
@@ -213,7 +245,7 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
-                 "n"(kUmmaTmemCols));
+                 "n"(umma_tmem_cols<H>()));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -225,12 +257,12 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
   tc05_after_sync();
   const uint32_t taddr = s_taddr;
   const uint32_t t_lane = taddr + (static_cast<uint32_t>(32 * warp) << 16);  // this warp's TMEM lanes
-  const uint32_t id32 = umma_idesc(32), id16 = umma_idesc(16);
+  const uint32_t idH = umma_idesc(H), id16 = umma_idesc(16);
   const uint32_t one_h = h2_bits(__floats2half2_rn(1.f, 0.f));
-  const float* s_b2 = reinterpret_cast<const float*>(s_w + UmmaLayout::B2);
-  const float* s_b3 = reinterpret_cast<const float*>(s_w + UmmaLayout::B3);
+  const float* s_b2 = reinterpret_cast<const float*>(s_w + UL::B2);
+  const float* s_b3 = reinterpret_cast<const float*>(s_w + UL::B3);
   const float dt = a.sys.dt;
-  const float dt3 = dt * *reinterpret_cast<const float*>(s_w + UmmaLayout::SC);  // dt 2^-s (exact)
+  const float dt3 = dt * *reinterpret_cast<const float*>(s_w + UL::SC);  // dt 2^-s (exact)
   const CostDev<float> cp = a.sys.cost;
   const float inv_s0 = 1.0f / a.sigma0, inv_s1 = 1.0f / a.sigma1;
   const float gml = a.gamma - a.lambda, half_lambda = 0.5f * a.lambda;
@@ -272,6 +304,7 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
     v1c = clamp_r(v1, a.sys.lo1, a.sys.hi1);
   };
 
+  cudaGridDependencySynchronize();  // x0 (written by the step graph's x0 fetch, whose programmatic dependent this is)
   const float* x0 = a.x0 + ctrl * 8;
   float px = x0[0], py = x0[1], th = x0[2];
   float roll = x0[3], vx = x0[4], vy = x0[5], thd = x0[6];
@@ -299,13 +332,13 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
   // one layer's MMAs by the elected thread: D_m = A_hi B_hi, D_c = A_hi B_lo + A_lo B_hi
   // (descriptors built once: A tiles and weight tiles never move)
   const uint64_t d_a1h = umma_desc(a1_hi), d_a1l = umma_desc(a1_lo);
-  const uint64_t d_a2h[2] = {umma_desc(a2_hi), umma_desc(a2_hi + kUmmaTileA)};
-  const uint64_t d_a2l[2] = {umma_desc(a2_lo), umma_desc(a2_lo + kUmmaTileA)};
-  const uint64_t d_w1h = umma_desc(w_addr + UmmaLayout::W1_HI), d_w1l = umma_desc(w_addr + UmmaLayout::W1_LO);
-  const uint64_t d_w2h[2] = {umma_desc(w_addr + UmmaLayout::W2_HI), umma_desc(w_addr + UmmaLayout::W2_HI + 1024)};
-  const uint64_t d_w2l[2] = {umma_desc(w_addr + UmmaLayout::W2_LO), umma_desc(w_addr + UmmaLayout::W2_LO + 1024)};
-  const uint64_t d_w3h[2] = {umma_desc(w_addr + UmmaLayout::W3_HI), umma_desc(w_addr + UmmaLayout::W3_HI + 512)};
-  const uint64_t d_w3l[2] = {umma_desc(w_addr + UmmaLayout::W3_LO), umma_desc(w_addr + UmmaLayout::W3_LO + 512)};
+  // (slice s of a tile sequence is its base descriptor + s * bytes / 16: the
+  // start-address field holds addr >> 4 and never carries out of 14 bits)
+  const uint64_t d_a2h = umma_desc(a2_hi), d_a2l = umma_desc(a2_lo);
+  const uint64_t d_w1h = umma_desc(w_addr + UL::W1_HI), d_w1l = umma_desc(w_addr + UL::W1_LO);
+  const uint64_t d_w2h = umma_desc(w_addr + UL::W2_HI), d_w2l = umma_desc(w_addr + UL::W2_LO);
+  const uint64_t d_w3h = umma_desc(w_addr + UL::W3_HI), d_w3l = umma_desc(w_addr + UL::W3_LO);
+  constexpr uint64_t kSliceA = kUmmaTileA >> 4, kSliceW2 = (32 * H) >> 4, kSliceW3 = 512 >> 4;
   auto sync_for_mma = [&] {
     proxy_fence_smem();
     tc05_before_sync();
@@ -315,40 +348,25 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
     sync_for_mma();
     if (tid == 0) {
       tc05_after_sync();
-      umma_f16(taddr, d_a1h, d_w1h, id32, 0);
-      umma_f16(taddr + 32, d_a1h, d_w1l, id32, 0);
-      umma_f16(taddr + 32, d_a1l, d_w1h, id32, 1);
+      umma_f16(taddr, d_a1h, d_w1h, idH, 0);
+      umma_f16(taddr + H, d_a1h, d_w1l, idH, 0);
+      umma_f16(taddr + H, d_a1l, d_w1h, idH, 1);
       umma_commit(mbar);
     }
   };
-  auto issue23 = [&](const uint64_t (&bh)[2], const uint64_t (&bl)[2], uint32_t idesc) {
+  auto issue23 = [&](uint64_t bh, uint64_t bl, uint64_t slice_w, uint32_t idesc) {
     sync_for_mma();
     if (tid == 0) {
       tc05_after_sync();
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        umma_f16(taddr, d_a2h[s], bh[s], idesc, s > 0);
-        umma_f16(taddr + 32, d_a2h[s], bl[s], idesc, s > 0);
-        umma_f16(taddr + 32, d_a2l[s], bh[s], idesc, 1);
+      for (int s = 0; s < NK; ++s) {
+        const uint64_t ah = d_a2h + s * kSliceA, al = d_a2l + s * kSliceA;
+        const uint64_t wh = bh + s * slice_w, wl = bl + s * slice_w;
+        umma_f16(taddr, ah, wh, idesc, s > 0);
+        umma_f16(taddr + H, ah, wl, idesc, s > 0);
+        umma_f16(taddr + H, al, wh, idesc, 1);
       }
       umma_commit(mbar);
-    }
-  };
-  // layer output (m + c [+ bias]) of this thread's row, 16 columns at a time
-  auto read_layer = [&](float (&y)[32], bool bias) {
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      float m16[16], c16[16];
-      tmem_ld16(t_lane + 16 * hh, m16);
-      tmem_ld16(t_lane + 32 + 16 * hh, c16);
-      tmem_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        float2 z = __fadd2_rn(make_float2(m16[j], m16[j + 1]), make_float2(c16[j], c16[j + 1]));
-        if (bias) z = __fadd2_rn(z, make_float2(s_b2[16 * hh + j], s_b2[16 * hh + j + 1]));
-        y[16 * hh + j] = z.x;
-        y[16 * hh + j + 1] = z.y;
-      }
     }
   };
   auto wait_mma = [&] {
@@ -384,20 +402,17 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
       p_coup = coup_t;
     }
     wait_mma();
-    float y[32];
-    read_layer(y, false);
-    umma_stage_act(y, a2_hi, a2_lo, tid);
-    issue23(d_w2h, d_w2l, id32);
+    umma_layer_to_a<H, SW, false>(t_lane, nullptr, a2_hi, a2_lo, tid);
+    issue23(d_w2h, d_w2l, kSliceW2, idH);
     produce_v(t + 1, !EVEN);
     wait_mma();
-    read_layer(y, true);
-    umma_stage_act(y, a2_hi, a2_lo, tid);  // (layer 2's MMAs have completed: the tiles are free)
-    issue23(d_w3h, d_w3l, id16);
+    umma_layer_to_a<H, SW, true>(t_lane, s_b2, a2_hi, a2_lo, tid);  // (layer 2's MMAs have completed: the tiles are free)
+    issue23(d_w3h, d_w3l, kSliceW3, id16);
     stage_v();  // v_{t+1} into the next step's layer-1 row (layer 1's tile is free)
     wait_mma();
     float om[4], oc[4];
     tmem_ld4(t_lane, om);
-    tmem_ld4(t_lane + 32, oc);
+    tmem_ld4(t_lane + H, oc);
     tmem_wait_ld();
     float d[4];
 #pragma unroll
@@ -434,7 +449,7 @@ __global__ void __launch_bounds__(kUmmaThreads, MPPI_UMMA_CTAS) rollout_umma_ker
   if (tid == 0) s_bad = 0;
   tc05_before_sync();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kUmmaTmemCols));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(umma_tmem_cols<H>()));
   if (valid && !isfinite(cost)) s_bad = 1;
   // rho = min, eta = sum exp(-(S - rho) / lambda) over the chunk (warps in order)
   Acc m = warp_min(valid ? cost : Acc(INFINITY));

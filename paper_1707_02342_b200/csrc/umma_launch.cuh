@@ -1,15 +1,18 @@
-// umma.cu — launcher of the tcgen05 / TMEM rollout (rollout_umma.cuh), H = 32.
+// umma_launch.cuh — launcher of the tcgen05 / TMEM rollout (rollout_umma.cuh)
+// for hidden width UMMA_H; instantiated by umma_h32.cu / umma_h64.cu so the
+// two widths build in parallel.
 #include "rollout_umma.cuh"
 #include "ws_launch.hpp"
 
 namespace mppi_host {
 namespace {
 
+constexpr int H = UMMA_H;
 template <int Mode, bool STAB, bool TRACE>
 cudaError_t go_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned char* wimg, int n_chunks, int ctrls,
                     cudaStream_t stream) {
-  auto kern = mppi_dev::rollout_umma_kernel<Mode, STAB, TRACE>;
-  const size_t smem = mppi_dev::umma_smem_bytes(a.T);
+  auto kern = mppi_dev::rollout_umma_kernel<H, Mode, STAB, TRACE>;
+  const size_t smem = mppi_dev::umma_smem_bytes<H>(a.T);
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -39,8 +42,9 @@ cudaError_t by_stab_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned c
 
 }  // namespace
 
-cudaError_t launch_rollout_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned char* wimg, int mode,
-                                int n_chunks, int ctrls, cudaStream_t stream) {
+template <>
+cudaError_t launch_rollout_umma<UMMA_H>(const mppi_dev::RolloutArgs<float>& a, const unsigned char* wimg, int mode,
+                                        int n_chunks, int ctrls, cudaStream_t stream) {
   switch (mode) {
     case mppi_dev::kInjected: return by_stab_umma<mppi_dev::kInjected>(a, wimg, n_chunks, ctrls, stream);
     case mppi_dev::kRefSplitmix: return by_stab_umma<mppi_dev::kRefSplitmix>(a, wimg, n_chunks, ctrls, stream);

@@ -42,10 +42,17 @@ extern template cudaError_t launch_tail_tc<32>(const mppi_dev::Acc*, int, int, l
                                                const mppi_dev::TailArgs&, int, bool, cudaStream_t);
 extern template cudaError_t launch_tail_tc<64>(const mppi_dev::Acc*, int, int, long long, double,
                                                const mppi_dev::TailArgs&, int, bool, cudaStream_t);
-// The tcgen05 / TMEM rollout (rollout_umma.cuh), H = 32: chunks of 128
+// The tcgen05 / TMEM rollout (rollout_umma.cuh), H = 32 or 64: chunks of 128
 // samples from a.chunk0; wimg is the weight image (umma_build_image).
+template <int H>
 cudaError_t launch_rollout_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned char* wimg, int mode,
                                 int n_chunks, int ctrls, cudaStream_t stream);
+template <>
+cudaError_t launch_rollout_umma<32>(const mppi_dev::RolloutArgs<float>&, const unsigned char*, int, int, int,
+                                    cudaStream_t);
+template <>
+cudaError_t launch_rollout_umma<64>(const mppi_dev::RolloutArgs<float>&, const unsigned char*, int, int, int,
+                                    cudaStream_t);
 // Fixed-group merge of the chunk partials (group.cuh): groups [g0, g0 + n_local)
 // of n_groups; programmatic dependent of the previous kernel when pdl.
 cudaError_t launch_group_merge(const mppi_dev::Acc* partials, long long partials_ctrl_stride, int n_chunks,

@@ -416,11 +416,11 @@ def test_full_iteration_parity_c1():
 
 
 def test_full_iteration_parity_c2():
-    """BASELINE c2 (K = 65536, T = 150, H = 64, tensor-core K1 with shared-
-    memory layer-2 fragments): two full iterations against the restatements."""
+    """BASELINE c2 (K = 65536, T = 150, H = 64, the tcgen05 / TMEM K1 by
+    default at this size): two full iterations against the restatements."""
     w = workload.make("c2")
     g, _ = pair(w, "fp32", "ref_splitmix")
-    assert "rollout_tc_kernel<f32,H=64" in g.kernel_variant
+    assert "rollout_umma_kernel<f32,H=64" in g.kernel_variant
     o32, o64 = _oracles(w, 64, w.costmap)
     iterate_against_oracles(g, o32, o64, w.x0[0].copy(), 2, threads=16, label="c2")
 
@@ -458,7 +458,7 @@ def test_fleet_member_parity_c3():
 
 
 def test_tcgen05_kernel_parity():
-    """The tcgen05 / TMEM K1 (rollout_umma.cuh, the default from 65 536 H = 32
+    """The tcgen05 / TMEM K1 (rollout_umma.cuh, the default from 32 768 H = 32
     samples; forced here at smaller K): per-sample costs, state trajectories
     and full iterations against the float and double restatements."""
     import os
@@ -477,6 +477,30 @@ def test_tcgen05_kernel_parity():
             assert np.allclose(g.rollout_states(w.x0[0], k), o32.rollout_states(w.x0[0], k), rtol=1e-5, atol=1e-5)
         g.plan, o32.plan, o64.plan = np.zeros_like(U), np.zeros_like(U), np.zeros_like(U)
         iterate_against_oracles(g, o32, o64, w.x0[0].copy(), 3, label="umma K=3000")
+    finally:
+        del os.environ["MPPI_KERNEL"]
+
+
+def test_tcgen05_kernel_parity_h64():
+    """The tcgen05 / TMEM K1 at H = 64 (four K slices per hidden layer, 128
+    TMEM columns): per-sample costs, a state trajectory and full iterations of
+    a c2-shaped controller (odd K, T = 150) against the restatements."""
+    import os
+    os.environ["MPPI_KERNEL"] = "umma"
+    try:
+        w = workload.make("c2", samples=2001)
+        g, _ = pair(w, "fp32", "ref_splitmix")
+        assert "rollout_umma_kernel<f32,H=64" in g.kernel_variant, g.kernel_variant
+        o32, o64 = _oracles(w, 64, w.costmap)
+        U = np.random.default_rng(7).uniform(-0.3, 0.3, (w.params.horizon_steps, 2))
+        g.plan, o32.plan = U, U
+        ok, flips, rel = compare_costs(g.rollout_batch(w.x0[0]), o32.rollout_batch(w.x0[0], threads=16),
+                                       COST_RTOL_FP32)
+        assert ok.mean() >= 0.999 and flips <= 2, (ok.mean(), flips, rel.max())
+        for k in (0, 1999):
+            assert np.allclose(g.rollout_states(w.x0[0], k), o32.rollout_states(w.x0[0], k), rtol=1e-5, atol=1e-5)
+        g.plan, o32.plan, o64.plan = np.zeros_like(U), np.zeros_like(U), np.zeros_like(U)
+        iterate_against_oracles(g, o32, o64, w.x0[0].copy(), 2, threads=16, label="umma H=64 K=2001")
     finally:
         del os.environ["MPPI_KERNEL"]
 

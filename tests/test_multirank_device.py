@@ -118,7 +118,7 @@ def test_fleet_controller_offset_is_the_global_index():
 
 @pytest.mark.parametrize("N", [2, 8])
 def test_local_shards_bit_identical_tcgen05_kernel(N):
-    """From 65 536 samples the H = 32 K1 is the tcgen05 / TMEM kernel (128
+    """From 32 768 samples the H = 32 K1 is the tcgen05 / TMEM kernel (128
     samples per CTA): the sharded iteration is still bit-identical to one GPU."""
     w = workload.make("c1", samples=70000)
     single, ranks = run_pair(w, N, steps=2)

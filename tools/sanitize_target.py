@@ -2,7 +2,7 @@
 """Small runs of every device kernel family for the device-checks build
 (tools/gpu_device_checks.sh; compute-sanitizer is closed on the GPU pool):
 the warp-pair K1 (c0 shape), the
-single-warp K1 with eps' on chip and regenerated (MT=1 / MT=2), the H=64 K1,
+single-warp K1 with eps' on chip and regenerated (MT=1 / MT=2), the tcgen05 K1, the H=64 K1,
 the FFMA2 and generic K1, fp64, the group merge, the tail (closed loop with
 the device plant), a local 2-rank shard, the CEM rule, the bicycle model and
 the parity kernels.  Short horizons keep the sanitizer run in minutes."""
@@ -37,7 +37,10 @@ run("c1", 4096, 20)                                   # MT=1, eps' on chip
 os.environ["MPPI_TC_STORE"] = "0"
 run("c1", 4096, 21)                                   # MT=1, regenerated eps', odd T
 del os.environ["MPPI_TC_STORE"]
-run("c4", 40000, 10, steps=1)                         # MT=2
+os.environ["MPPI_KERNEL"] = "mma"
+run("c4", 40000, 10, steps=1)                         # MT=2 (mma.sync forced: tcgen05 is the default here)
+del os.environ["MPPI_KERNEL"]
+run("c4", 40000, 10, steps=1)                         # tcgen05 / TMEM K1
 run("c2", 2048, 12)                                   # H=64
 os.environ["MPPI_KERNEL"] = "ws"
 run("c1", 2048, 12)                                   # FFMA2 K1
