@@ -379,6 +379,8 @@ def run_ours(args):
     sfu_frac = (xu_per_ss * k_local * T / (k1_avg_ms * 1e-3) / (mufu_gops * 1e9)) \
         if (xu_per_ss and k1_avg_ms > 0 and mufu_gops > 0) else None
     tensor_peak = hmma_tflops / 3.0  # three fp16 products (hi*hi + hi*lo + lo*hi) per fp32 MAC
+    tc05_peak = measured_bf16_tflops()
+    tc05_peak = tc05_peak / 3.0 if tc05_peak else None
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         shape1 = dict(shape)
@@ -403,7 +405,7 @@ def run_ours(args):
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": ncu.get("dram_bytes_per_launch") if same_shape else None,
-                     "kernel": "rollout_tc_kernel (K1)", "k1_ms_per_launch": k1_avg_ms,
+                     "kernel": ctrl.kernel_variant.split("<")[0] + " (K1)", "k1_ms_per_launch": k1_avg_ms,
                      "k1_share_of_step": k1_avg_ms / ms_per_step if ms_per_step else None,
                      "flop_per_launch": k1_flops, "flop_per_sample_step": flop_unit,
                      "peak_source": "measured FFMA/FFMA2 probe on this GPU (mppi_gpu_fp32_peak_probe); "
@@ -412,6 +414,10 @@ def run_ours(args):
                          "tensor_mma_f16x3": {"peak_tflops": tensor_peak, "frac": achieved / tensor_peak
                                               if (achieved and tensor_peak) else None,
                                               "note": "measured mma.sync m16n8k16 f16 peak / 3 (the fp16x3 split)"},
+                         "tensor_tcgen05_f16x3": {"peak_tflops": tc05_peak, "frac": achieved / tc05_peak
+                                                  if (achieved and tc05_peak) else None,
+                                                  "note": "MEASURED_PEAKS.json dense bf16 (cuBLAS, tcgen05) / 3 "
+                                                          "(the fp16x3 split); the ceiling of rollout_umma_kernel"},
                          "sfu": {"peak_gops": mufu_gops, "xu_lane_ops_per_sample_step": xu_per_ss, "frac": sfu_frac,
                                  "note": "XU instructions per sample-step from the ncu capture x K1 units / K1 time "
                                          "vs the measured MUFU ex2 peak"},
@@ -424,6 +430,16 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if pg:
         pg.destroy_process_group()
+
+
+def measured_bf16_tflops():
+    """Dense bf16 tensor peak of this pool's B200s (driver-written
+    MEASURED_PEAKS.json, cuBLAS = tcgen05 kind::f16 rate), or None."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def main():

@@ -2,7 +2,9 @@
 # Round evidence for profiles/<TAG>/: bench lines (c1 with the CPU baseline,
 # the reference arm, c0/c2/c3), the ncu launch list of the c1 bench command,
 # one ncu --set full capture each of K1, the group merge and the tail at c1,
-# the config sweep and the accuracy study.   Usage: bash tools/gpu_evidence.sh TAG
+# of the tcgen05 K1 at c2 (H = 64) and K = 262144 (H = 32) with the mma.sync
+# K1 beside them, the config sweep and the accuracy study.
+# Usage: bash tools/gpu_evidence.sh TAG
 TAG=${1:-r02}
 O=gpurun_out/$TAG
 mkdir -p $O
@@ -23,7 +25,11 @@ for k in rollout group_merge tail_kernel; do
   ncu -i $O/ncu_full_${k}_c1.ncu-rep --page details --csv > $O/ncu_full_${k}_c1_details.csv 2>&1
 done
 ncu -i $O/ncu_full_rollout_c1.ncu-rep --page source --csv --print-source sass > $O/ncu_full_rollout_c1_source.csv 2>&1
-timeout 900 python tools/sweep.py envs '[["c0",1920,{}],["c1",16384,{}],["c2",65536,{}],["c4",1024,{}],["c4",4096,{}],["c4",65536,{}],["c4",262144,{}],["c4",1048576,{}]]' > $O/sweep_configs.jsonl 2>&1
+bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_umma > /dev/null 2>&1
+bash tools/gpu_ncu_full.sh $TAG c4 262144 rollout_umma > /dev/null 2>&1
+MPPI_KERNEL=mma bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_tc > /dev/null 2>&1
+MPPI_KERNEL=mma bash tools/gpu_ncu_full.sh $TAG c4 262144 rollout_tc > /dev/null 2>&1
+timeout 900 python tools/sweep.py envs '[["c0",1920,{}],["c1",16384,{}],["c2",65536,{}],["c4",1024,{}],["c4",4096,{}],["c4",32768,{}],["c4",65536,{}],["c4",262144,{}],["c4",1048576,{}],["c2",65536,{"MPPI_KERNEL":"mma"}],["c4",32768,{"MPPI_KERNEL":"mma"}],["c4",262144,{"MPPI_KERNEL":"mma"}],["c4",1048576,{"MPPI_KERNEL":"mma"}]]' > $O/sweep_configs.jsonl 2>&1
 timeout 1200 python tools/accuracy.py c0,c1 > $O/accuracy.jsonl 2>&1
 rm -f $O/*.ncu-rep.tmp
 cat $O/bench_c1.json | cut -c1-600
