@@ -98,6 +98,16 @@ __device__ __forceinline__ float tc_ld_opaque(const uint32_t* p) {
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
+// st.shared.b32 under a predicate, at a shared-window address: the owners'
+// stage stores stay predicated instructions (a C++ `if` around them compiled
+// to a branch with a reconvergence point in every step), and the address
+// needs no generic-to-shared conversion inside the step loop
+__device__ __forceinline__ void sts32_if(uint32_t addr, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}" ::"r"(addr), "r"(v),
+               "r"(static_cast<int>(p))
+               : "memory");
+}
+
 // (x, y) -> fp16x2 hi and lo words: hi = fp16(x), lo = fp16(x - hi).
 __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x, y);
@@ -356,7 +366,11 @@ template <int H, int MT>
 __host__ __device__ constexpr int tc_min_ctas() {
   return (MT == 2 || H == 32) ? 3 : 2;
 }
-template <int H, int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE>
+// PST: the owners' stage stores as predicated st.shared (sts32_if) instead of
+// a C++ `if` (a branch and a reconvergence point per step): measured -7 % K1
+// at <= 1 warp per scheduler (K = 4096, 8192), +1 % at c1's 1.7 (tc_launch.cuh
+// picks it by the grid size; same arithmetic, bit-identical results).
+template <int H, int MT, int NW, int Mode, bool STAB, bool STORE, bool TRACE, bool PST = false>
 __global__ void __launch_bounds__(32 * NW, tc_min_ctas<H, MT>()) rollout_tc_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                             const uint32_t* __restrict__ frag) {
   constexpr int CH = 16 * MT;
@@ -507,6 +521,11 @@ __global__ void __launch_bounds__(32 * NW, tc_min_ctas<H, MT>()) rollout_tc_kern
   MapTaps<float> q{};
   float p_roll = 0.f, p_vx = 0.f, p_vy = 0.f, p_coup = 0.f;
   const bool trace = a.trace_states != nullptr && valid && k == a.trace_k;
+  // this lane's stage-input words (shared-window byte addresses)
+  const uint32_t s_in_hi = static_cast<uint32_t>(__cvta_generic_to_shared(&st.in[m_own][0][0]));
+  const uint32_t s_in_lo = static_cast<uint32_t>(__cvta_generic_to_shared(&st.in[m_own][1][0]));
+  const uint32_t w_in0 = 4u * tc_in_word(g, 0, t4 & 1), w_in1 = 4u * tc_in_word(g, 1, t4 & 1),
+                 w_in2 = 4u * tc_in_word(g, 2, t4 & 1);
   produce_v(0, true);
 
   // One step; EVEN = parity of t (compile-time, so the Philox draw of the
@@ -526,14 +545,21 @@ __global__ void __launch_bounds__(32 * NW, tc_min_ctas<H, MT>()) rollout_tc_kern
     // mirror lanes compute the same values and store nothing, so no two
     // lanes write one word and no branch splits the step's basic block)
     {
-      uint32_t* hi_plane = st.in[m_own][0];
-      uint32_t* lo_plane = st.in[m_own][1];
-      const int h = t4 & 1;
       uint32_t hi0, lo0, hi1, lo1, hi2, lo2;
       split2(roll, vx, hi0, lo0);
       split2(vy, thd, hi1, lo1);
       split2(v0c, v1c, hi2, lo2);
-      if (!dup) {
+      if constexpr (PST) {
+        sts32_if(s_in_hi + w_in0, hi0, !dup);
+        sts32_if(s_in_lo + w_in0, lo0, !dup);
+        sts32_if(s_in_hi + w_in1, hi1, !dup);
+        sts32_if(s_in_lo + w_in1, lo1, !dup);
+        sts32_if(s_in_hi + w_in2, hi2, !dup);
+        sts32_if(s_in_lo + w_in2, lo2, !dup);
+      } else if (!dup) {
+        uint32_t* hi_plane = st.in[m_own][0];
+        uint32_t* lo_plane = st.in[m_own][1];
+        const int h = t4 & 1;
         hi_plane[tc_in_word(g, 0, h)] = hi0;
         lo_plane[tc_in_word(g, 0, h)] = lo0;
         hi_plane[tc_in_word(g, 1, h)] = hi1;

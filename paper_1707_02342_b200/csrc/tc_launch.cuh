@@ -32,10 +32,10 @@ cudaError_t launch_k1(Kern kern, dim3 grid, int threads, size_t smem, cudaStream
   return cudaLaunchKernelEx(&cfg, kern, a, frag);
 }
 
-template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE>
+template <int H, int MT, int Mode, bool STAB, bool STORE, bool TRACE, bool PST = false>
 cudaError_t go_trace(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls, size_t smem,
                      cudaStream_t stream) {
-  auto kern = mppi_dev::rollout_tc_kernel<H, MT, kTcWarps, Mode, STAB, STORE, TRACE>;
+  auto kern = mppi_dev::rollout_tc_kernel<H, MT, kTcWarps, Mode, STAB, STORE, TRACE, PST>;
   // (static + dynamic shared memory may pass 48 KB even when `smem` does not:
   // the H = 64 kernel holds its layer-2 fragments in 16 KB of static smem)
   {
@@ -52,6 +52,18 @@ cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
   // (a trace is a parity call: no on-chip eps' variant is compiled for it)
   if constexpr (!STORE) {
     if (a.trace_states) return go_trace<H, MT, Mode, STAB, false, true>(a, frag, n_chunks, ctrls, smem, stream);
+  }
+  // predicated stage stores at <= 1 warp per scheduler (H = 32, MT = 1;
+  // rollout_tc_kernel's PST), the C++ branch above that
+  if constexpr (H == 32 && MT == 1) {
+    static const int schedulers = [] {
+      int dev = 0, n = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return 4 * n;
+    }();
+    if (static_cast<long long>(n_chunks) * ctrls <= schedulers)
+      return go_trace<H, MT, Mode, STAB, STORE, false, true>(a, frag, n_chunks, ctrls, smem, stream);
   }
   return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, n_chunks, ctrls, smem, stream);
 }
