@@ -68,15 +68,17 @@ cudaError_t go_store(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag
   return go_trace<H, MT, Mode, STAB, STORE, false>(a, frag, n_chunks, ctrls, smem, stream);
 }
 // The warp-pair kernel (rollout_tc_pair.cuh): H = 32, eps' on chip, no trace.
-// Used by default only at no more than one chunk per SM (c0: K1 -5 %); with
-// more chunks per SM its barrier handoffs cost more than the shorter per-warp
-// chain saves (c1: +24 %, profiles/README.md).  MPPI_TC_PAIR=1 forces it (when
-// its grid is resident at once), MPPI_TC_PAIR=0 disables it.
+// Opt-in (MPPI_TC_PAIR=1, when its grid is resident at once): it was the
+// default at <= 1 chunk per SM (c0: K1 -5 % against the branch-store
+// single-warp kernel) until the single-warp kernel's predicated stage stores
+// (PST) made that kernel faster there too (c0 K1 89.7 -> 87.2 us); with more
+// chunks per SM its barrier handoffs cost more than the shorter per-warp
+// chain saves (c1: +24 %, profiles/README.md).
 constexpr int kTcPairs = 1;  // warp pairs (chunks) per CTA
 template <int Mode, bool STAB>
 bool pair_fits(int T, int n_chunks, int ctrls) {
   const char* e = std::getenv("MPPI_TC_PAIR");
-  if (e && std::atoi(e) == 0) return false;
+  if (!e || std::atoi(e) == 0) return false;
   auto kern = mppi_dev::rollout_tc_pair_kernel<kTcPairs, Mode, STAB>;
   const size_t smem = mppi_dev::tc_pair_smem_bytes(T, kTcPairs);
   int dev = 0, sms = 0, per_sm = 0;

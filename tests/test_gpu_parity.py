@@ -549,7 +549,7 @@ def test_kernel_variant_and_launch_count():
     g.mpc_step(w.x0[0])
     # the fp32 H = 32 vehicle step: the x0 fetch, the tensor-core K1 (its
     # programmatic dependent), the group merge and the tail
-    assert "rollout_tc_pair_kernel" in g.kernel_variant  # one wave at this size: the warp-pair K1
+    assert "rollout_tc_kernel<f32,H=32,MT=1" in g.kernel_variant  # one warp per 16-sample chunk
     assert g.launch_count - n0 == 4
     w64 = workload.make("c2", samples=256, horizon_steps=20)
     g64, _ = pair(w64, "fp32", "philox")

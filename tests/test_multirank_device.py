@@ -53,7 +53,8 @@ def run_pair(w, N, prec="fp32", noise="philox", steps=3):
 @pytest.mark.parametrize("K", [16384, 5000, 1920, 100])
 @pytest.mark.parametrize("N", [2, 4, 8])
 def test_local_shards_bit_identical_to_one_gpu_fp32(K, N):
-    """Tensor-core path: c1 size, ragged K, c0 size (warp-pair K1 per rank), and
+    """Tensor-core path: c1 size (the single GPU with branch-form stage stores, the ranks with
+    predicated ones), ragged K, c0 size, and
     K = 100 (7 chunks for 8 groups: empty groups and ranks without samples)."""
     w = workload.make("c1", samples=K)
     single, ranks = run_pair(w, N)

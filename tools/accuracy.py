@@ -74,7 +74,7 @@ def one(cfg, iters):
     print(json.dumps({"cfg": cfg, "kernel": g.kernel_variant, "max": agg, "per_iteration": rows}), flush=True)
 
 
-VARIANTS = [{}, {"MPPI_TC_W3_SHIFT": "0"}, {"MPPI_TC_PAIR": "0"}, {"MPPI_KERNEL": "ws"}]
+VARIANTS = [{}, {"MPPI_TC_W3_SHIFT": "0"}, {"MPPI_TC_PAIR": "1"}, {"MPPI_KERNEL": "ws"}]
 
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "one":

@@ -32,7 +32,10 @@ def run(cfg, K, T, steps=2, **kw):
     return c, w
 
 
-run("c0", 1920, 20)                                   # warp-pair K1, one wave
+os.environ["MPPI_TC_PAIR"] = "1"
+run("c0", 1920, 20)                                   # warp-pair K1 (opt-in), one wave
+del os.environ["MPPI_TC_PAIR"]
+run("c0", 1920, 20)                                   # single-warp K1, predicated stage stores
 run("c1", 4096, 20)                                   # MT=1, eps' on chip
 os.environ["MPPI_TC_STORE"] = "0"
 run("c1", 4096, 21)                                   # MT=1, regenerated eps', odd T
