@@ -39,19 +39,35 @@ __host__ __device__ constexpr int umma_sw_rcp() {
   return H == 32 ? 10 : 0;
 #endif
 }
-// resident CTAs per SM the register budget is sized for (H = 64: three, the
-// shared-memory footprint allows no more)
+// 128-sample tiles per CTA (default one).  With two, a CTA runs two
+// independent MMA pipelines (256 threads, a named barrier per tile) sharing
+// ONE shared-memory copy of the weights: at H = 64 the weights are 24 KB of
+// the 66 KB per-tile footprint, so CTA pairs hold four tiles per SM where
+// single-tile CTAs fit three.  Measured (-DMPPI_UMMA_TPC=2, H = 64, 128
+// registers): c2 K1 1165 -> 1118 us (one wave instead of 1.15), but
+// K = 32768 +17 % and K = 131072 +13 % — kept as a build option.
+template <int H>
+__host__ __device__ constexpr int umma_tiles_per_cta() {
+#ifdef MPPI_UMMA_TPC
+  return MPPI_UMMA_TPC;
+#else
+  return 1;
+#endif
+}
+// resident CTAs per SM the register budget is sized for: four tiles at H = 32
+// (128 registers), three at H = 64 (its shared-memory footprint allows no
+// more), two two-tile CTAs
 template <int H>
 __host__ __device__ constexpr int umma_min_ctas() {
 #ifdef MPPI_UMMA_CTAS
   return MPPI_UMMA_CTAS;
 #else
-  return H == 32 ? 4 : 3;
+  return umma_tiles_per_cta<H>() == 2 ? 2 : (H == 32 ? 4 : 3);
 #endif
 }
-// accumulators: [0, H) hi*hi, [H, 2H) cross terms
+// accumulators per tile: [0, H) hi*hi, [H, 2H) cross terms
 template <int H>
-__host__ __device__ constexpr int umma_tmem_cols() { return 2 * H; }
+__host__ __device__ constexpr int umma_tmem_cols() { return 2 * H * umma_tiles_per_cta<H>(); }
 
 // Byte offset of element (row, k) of a K = 16 fp16 tile in the canonical
 // K-major, no-swizzle layout: 8-row x 16-byte core matrices, the two K halves
@@ -187,33 +203,51 @@ __device__ __forceinline__ void umma_layer_to_a(uint32_t t_lane, const float* __
   }
 }
 
-// grid = (chunks of 128 samples, controllers), block = 128.  Dynamic smem:
-// plan (2T + 2 floats) | weight image (UmmaLayout<H>) | A tiles: layer 1 hi/lo
-// (2 x 4 KB), layers 2/3 hi/lo x H/16 K slices | numerator staging
-// (kTcTB x 2 x 128 doubles, aliased on the A tiles after the rollout).
+// grid = (ceil(chunks / TPC), controllers), block = 128 TPC, tile i of a CTA
+// = chunk blockIdx.x TPC + i of 128 samples.  Dynamic smem: plan (2T + 2
+// floats) | weight image (UmmaLayout<H>) | per tile: A tiles: layer 1 hi/lo
+// (2 x 4 KB), layers 2/3 hi/lo x H/16 K slices, with the numerator staging
+// (kTcTB x 2 x 128 doubles) aliased on them after the rollout.
+template <int H>
+__host__ __device__ constexpr size_t umma_tile_region_bytes() {
+  const size_t tiles = (2 + 2 * (H / 16)) * kUmmaTileA;
+  const size_t stage = sizeof(double) * kTcTB * 2 * kUmmaThreads;
+  return tiles > stage ? tiles : stage;
+}
 template <int H>
 __host__ __device__ constexpr size_t umma_smem_bytes(int T) {
   const size_t plan = (sizeof(float) * (2 * T + 2) + 127) & ~size_t(127);
-  const size_t tiles = (2 + 2 * (H / 16)) * kUmmaTileA;
-  const size_t stage = sizeof(double) * kTcTB * 2 * kUmmaThreads;
-  return plan + UmmaLayout<H>::BYTES + (tiles > stage ? tiles : stage) + 128;
+  return plan + UmmaLayout<H>::BYTES + umma_tiles_per_cta<H>() * umma_tile_region_bytes<H>() + 128;
+}
+// a named barrier over the 128 threads of tile `tile` (ids 1 ..; 0 is __syncthreads)
+__device__ __forceinline__ void umma_tile_bar(int tile) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + tile), "n"(kUmmaThreads) : "memory");
 }
 
 template <int H, int Mode, bool STAB, bool TRACE>
-__global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma_kernel(const __grid_constant__ RolloutArgs<float> a,
-                                                                       const unsigned char* __restrict__ wimg) {
+__global__ void __launch_bounds__(kUmmaThreads * umma_tiles_per_cta<H>(), umma_min_ctas<H>()) rollout_umma_kernel(
+    const __grid_constant__ RolloutArgs<float> a, const unsigned char* __restrict__ wimg) {
+  constexpr int TPC = umma_tiles_per_cta<H>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_taddr;
-  __shared__ __align__(8) unsigned long long s_mbar;
-  __shared__ double s_red[kUmmaThreads / 32];
-  __shared__ int s_bad;
+  __shared__ __align__(8) unsigned long long s_mbar_all[TPC];
+  __shared__ double s_red_all[TPC][kUmmaThreads / 32];
+  __shared__ int s_bad_all[TPC];
   const int T = a.T;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // tid: this thread's row (sample) of its tile; warp: its warp within the
+  // tile (= its TMEM lane quarter)
+  const int tile = TPC == 1 ? 0 : static_cast<int>(threadIdx.x) / kUmmaThreads;
+  const int tid = TPC == 1 ? static_cast<int>(threadIdx.x) : static_cast<int>(threadIdx.x) % kUmmaThreads;
+  const int warp = tid >> 5, lane = tid & 31;
   const int ctrl = blockIdx.y;
   if (a.abort_flag[static_cast<size_t>(ctrl) * a.abort_stride] != 0) return;
-  const int chunk = a.chunk0 + blockIdx.x;
+  const int chunk = a.chunk0 + blockIdx.x * TPC + tile;
+  // a tile past the rank's last chunk (last CTA only) runs without writing
+  const bool active = TPC == 1 || chunk < a.chunk_end;  // (single-tile grids hold exactly the rank's chunks)
   const int k = chunk * kUmmaThreads + tid;
-  const bool valid = k < a.K;
+  const bool valid = active && k < a.K;
+  double* s_red = s_red_all[tile];
+  int& s_bad = s_bad_all[tile];
   const bool zm = k >= a.zero_start;
   const int kn = valid ? k : 0;
 
@@ -224,25 +258,26 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
   constexpr int SW = umma_sw_rcp<H>();
   unsigned char* s_tiles = s_w + UL::BYTES;
   s_tiles = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(s_tiles) + 127) & ~uintptr_t(127));
+  s_tiles += static_cast<size_t>(tile) * umma_tile_region_bytes<H>();
   const uint32_t w_addr = static_cast<uint32_t>(__cvta_generic_to_shared(s_w));
   const uint32_t a1_hi = static_cast<uint32_t>(__cvta_generic_to_shared(s_tiles));
   const uint32_t a1_lo = a1_hi + kUmmaTileA;
   const uint32_t a2_hi = a1_lo + kUmmaTileA;        // NK K slices
   const uint32_t a2_lo = a2_hi + NK * kUmmaTileA;   // NK K slices
-  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar_all[tile]));
 
-  for (int i = tid; i < 2 * T + 2; i += kUmmaThreads)
+  for (int i = threadIdx.x; i < 2 * T + 2; i += kUmmaThreads * TPC)
     s_plan[i] = (i < 2 * T) ? a.plan[static_cast<size_t>(ctrl) * 2 * T + i] : 0.f;
   {
     const uint4* src = reinterpret_cast<const uint4*>(wimg);
     uint4* dst = reinterpret_cast<uint4*>(s_w);
-    for (int i = tid; i < static_cast<int>(UL::BYTES / 16); i += kUmmaThreads) dst[i] = src[i];
+    for (int i = threadIdx.x; i < static_cast<int>(UL::BYTES / 16); i += kUmmaThreads * TPC) dst[i] = src[i];
   }
   // the constant-one input (k = 6, the layer-1 bias column) and the zero K
   // half (k = 8 .. 15) of this thread's layer-1 rows, written once
   sts128(a1_hi + umma_tile_offset(tid, 8), 0u, 0u, 0u, 0u);
   sts128(a1_lo + umma_tile_offset(tid, 8), 0u, 0u, 0u, 0u);
-  if (warp == 0) {
+  if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
                  "n"(umma_tmem_cols<H>()));
@@ -255,7 +290,7 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
   tc05_before_sync();
   __syncthreads();
   tc05_after_sync();
-  const uint32_t taddr = s_taddr;
+  const uint32_t taddr = s_taddr + static_cast<uint32_t>(2 * H * tile);  // this tile's accumulator columns
   const uint32_t t_lane = taddr + (static_cast<uint32_t>(32 * warp) << 16);  // this warp's TMEM lanes
   const uint32_t idH = umma_idesc(H), id16 = umma_idesc(16);
   const uint32_t one_h = h2_bits(__floats2half2_rn(1.f, 0.f));
@@ -342,7 +377,8 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
   auto sync_for_mma = [&] {
     proxy_fence_smem();
     tc05_before_sync();
-    __syncthreads();
+    if constexpr (TPC == 1) __syncthreads();
+    else umma_tile_bar(tile);
   };
   auto issue1 = [&] {
     sync_for_mma();
@@ -449,7 +485,8 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
   if (tid == 0) s_bad = 0;
   tc05_before_sync();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(umma_tmem_cols<H>()));
+  if (threadIdx.x < 32)  // (the allocating warp frees every tile's columns)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "n"(umma_tmem_cols<H>()));
   if (valid && !isfinite(cost)) s_bad = 1;
   // rho = min, eta = sum exp(-(S - rho) / lambda) over the chunk (warps in order)
   Acc m = warp_min(valid ? cost : Acc(INFINITY));
@@ -465,8 +502,8 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
   __syncthreads();
   Acc* out = a.partials + static_cast<size_t>(ctrl) * a.partials_ctrl_stride +
              static_cast<size_t>(chunk) * a.partial_stride;
-  MPPI_DCHECK(static_cast<long long>(chunk + 1) * a.partial_stride <= a.partials_ctrl_stride);
-  if (tid == 0) {
+  MPPI_DCHECK(!active || static_cast<long long>(chunk + 1) * a.partial_stride <= a.partials_ctrl_stride);
+  if (tid == 0 && active) {
     Acc eta = s_red[0];
 #pragma unroll
     for (int w = 1; w < kUmmaThreads / 32; ++w) eta = eta + s_red[w];
@@ -505,7 +542,7 @@ __global__ void __launch_bounds__(kUmmaThreads, umma_min_ctas<H>()) rollout_umma
       const Acc s1 = __shfl_xor_sync(0xffffffffu, s, 1);
       const Acc s2 = __shfl_xor_sync(0xffffffffu, s, 2);
       const Acc s3 = __shfl_xor_sync(0xffffffffu, s, 3);
-      if (qs == 0 && tb + (e >> 1) < T) {
+      if (qs == 0 && active && tb + (e >> 1) < T) {
         // stripes 0, 1, 2, 3 of element e live in lanes 4e' .. 4e' + 3 of this warp
         out[kPartialHeader + 2 * tb + e] = __dadd_rn(__dadd_rn(s, s1), __dadd_rn(s2, s3));
       }

@@ -16,8 +16,9 @@ cudaError_t go_umma(const mppi_dev::RolloutArgs<float>& a, const unsigned char* 
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_chunks, ctrls);
-  cfg.blockDim = dim3(mppi_dev::kUmmaThreads);
+  constexpr int TPC = mppi_dev::umma_tiles_per_cta<H>();
+  cfg.gridDim = dim3((n_chunks + TPC - 1) / TPC, ctrls);
+  cfg.blockDim = dim3(mppi_dev::kUmmaThreads * TPC);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
