@@ -29,7 +29,7 @@ bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_umma > /dev/null 2>&1
 bash tools/gpu_ncu_full.sh $TAG c4 262144 rollout_umma > /dev/null 2>&1
 MPPI_KERNEL=mma bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_tc > /dev/null 2>&1
 MPPI_KERNEL=mma bash tools/gpu_ncu_full.sh $TAG c4 262144 rollout_tc > /dev/null 2>&1
-timeout 900 python tools/sweep.py envs '[["c0",1920,{}],["c1",16384,{}],["c2",65536,{}],["c4",1024,{}],["c4",4096,{}],["c4",32768,{}],["c4",65536,{}],["c4",262144,{}],["c4",1048576,{}],["c2",65536,{"MPPI_KERNEL":"mma"}],["c4",32768,{"MPPI_KERNEL":"mma"}],["c4",262144,{"MPPI_KERNEL":"mma"}],["c4",1048576,{"MPPI_KERNEL":"mma"}]]' > $O/sweep_configs.jsonl 2>&1
+timeout 900 python tools/sweep.py envs '[["c0",1920,{}],["c1",16384,{}],["c2",65536,{}],["c4",1024,{}],["c4",4096,{}],["c4",8192,{}],["c4",16384,{}],["c4",32768,{}],["c4",65536,{}],["c4",262144,{}],["c4",1048576,{}],["c2",65536,{"MPPI_KERNEL":"mma"}],["c4",32768,{"MPPI_KERNEL":"mma"}],["c4",262144,{"MPPI_KERNEL":"mma"}],["c4",1048576,{"MPPI_KERNEL":"mma"}]]' > $O/sweep_configs.jsonl 2>&1
 timeout 1200 python tools/accuracy.py c0,c1 > $O/accuracy.jsonl 2>&1
 rm -f $O/*.ncu-rep.tmp
 cat $O/bench_c1.json | cut -c1-600
