@@ -45,6 +45,9 @@ run("c4", 40000, 10, steps=1)                         # MT=2 (mma.sync forced: t
 del os.environ["MPPI_KERNEL"]
 run("c4", 40000, 10, steps=1)                         # tcgen05 / TMEM K1
 run("c2", 2048, 12)                                   # H=64
+os.environ["MPPI_KERNEL"] = "umma"
+run("c2", 2001, 12)                                   # tcgen05 K1 at H=64, ragged last tile
+del os.environ["MPPI_KERNEL"]
 os.environ["MPPI_KERNEL"] = "ws"
 run("c1", 2048, 12)                                   # FFMA2 K1
 del os.environ["MPPI_KERNEL"]
