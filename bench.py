@@ -354,8 +354,9 @@ def run_ours(args):
         e_ms = float(max_over_ranks([ev0.elapsed_time(ev1)])[0])
         e2e = {"value": units_per_step * args.steps / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms / args.steps,
                "h2d_bytes_per_step": C * 8 * 4, "d2h_bytes_per_step": C * 96,
-               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): x0 pinned H2D, graph replay, status D2H "
-                       "(written to pinned host memory by the tail kernel)"}
+               "path": "Controller.mpc_step -> mppi_gpu_step (C ABI): graph replay whose first kernel reads x0 "
+                       "from pinned host memory (H2D over PCIe), status D2H written to pinned host memory by the "
+                       "tail kernel; the host waits on its sequence word"}
 
     if rank != 0:
         if pg:
