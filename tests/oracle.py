@@ -340,3 +340,48 @@ def step_basis(x, v, dt, theta):
                                  p(np.ascontiguousarray(v, dtype=np.float64)), dt,
                                  p(np.ascontiguousarray(theta, dtype=np.float64).reshape(100)), p(out)))
     return out
+
+
+# ---------------------------------------------------------------- LQ oracle
+def _require_psd(M, what):
+    """require_psd (verification.cpp): symmetric and positive semidefinite."""
+    M = np.asarray(M, dtype=np.float64)
+    if not np.allclose(M, M.T, rtol=0.0, atol=1e-12) or np.linalg.eigvalsh(0.5 * (M + M.T)).min() < -1e-12:
+        raise OracleInvalidArgument(-1, f"{what} must be symmetric positive semidefinite")
+    return M
+
+
+def riccati_plan(A, B, Q, Qf, R, T, x0):
+    """riccati_plan (verification.cpp:72-99): backward Riccati recursion
+    K_t = (R + B'PB)^-1 B'PA, P <- Q + A'P(A - B K_t) from P = Qf, then the
+    forward rollout u_t = -K_t x_t.  Returns the T x m plan."""
+    A, B = np.asarray(A, dtype=np.float64), np.asarray(B, dtype=np.float64)
+    Q, Qf, R = _require_psd(Q, "riccati_plan: Q"), _require_psd(Qf, "riccati_plan: Qf"), _require_psd(R, "riccati_plan: R")
+    if np.linalg.eigvalsh(R).min() <= 0.0:
+        raise OracleInvalidArgument(-1, "riccati_plan: R must be positive definite")
+    gains = [None] * T
+    P = Qf
+    for t in range(T - 1, -1, -1):
+        BtP = B.T @ P
+        gains[t] = np.linalg.solve(R + BtP @ B, BtP @ A)
+        P = Q + A.T @ P @ (A - B @ gains[t])
+    plan = np.zeros((T, B.shape[1]))
+    x = np.asarray(x0, dtype=np.float64)
+    for t in range(T):
+        u = -gains[t] @ x
+        plan[t] = u
+        x = A @ x + B @ u
+    return plan
+
+
+def lqr_oracle(A, B, Q, Qf, sigma_diag, lam, T, x0):
+    """lqr_oracle (verification.cpp:101-108): the running cost lands on the
+    post-step states, so x_T carries Q + Qf; the sampling optimizer's control
+    penalty with gamma = lambda is R = (lambda / 2) Sigma^-1."""
+    if not lam > 0.0:
+        raise OracleInvalidArgument(-1, "LQInstance: lambda must be > 0")
+    sig = np.asarray(sigma_diag, dtype=np.float64)
+    if sig.min() <= 0.0:
+        raise OracleInvalidArgument(-1, "LQInstance: sigma entries must be > 0")
+    R = np.diag(lam / 2.0 / sig)
+    return riccati_plan(A, B, Q, np.asarray(Q) + np.asarray(Qf), R, T, x0)
