@@ -505,6 +505,29 @@ def test_tcgen05_kernel_parity_h64():
         del os.environ["MPPI_KERNEL"]
 
 
+@pytest.mark.parametrize("H", [32, 64])
+def test_tcgen05_kernel_injected_noise(H):
+    """The north star's parity method on the tcgen05 K1 at a size where it is
+    the default (K = 33001 >= 32 768, a ragged last tile): the reference's own
+    seeded noise buffer (sample_perturbations, sampler.cpp:5-39) injected,
+    every per-sample cost within rtol 1e-5 of the float restatement and the
+    stored batch (eps - U for the zero-mean samples, controller.cpp:70-72)
+    identical."""
+    w = workload.make("c1" if H == 32 else "c2", samples=33001, horizon_steps=20)
+    g, o = pair(w, "fp32", "injected")
+    assert f"rollout_umma_kernel<f32,H={H}" in g.kernel_variant, g.kernel_variant
+    eps, _ = oracle.sample_perturbations(w.params.samples, w.params.horizon_steps, w.params.sigma_diag,
+                                         w.params.explore_fraction, w.params.seed, 0)
+    U = np.random.default_rng(11).uniform(-0.3, 0.3, (w.params.horizon_steps, 2))
+    g.plan, o.plan = U, U
+    dc, dstored = g.rollout_batch(w.x0[0], eps, return_batch=True)
+    oc, ostored = o.rollout_batch(w.x0[0], eps, threads=16, return_batch=True)
+    ok, flips, rel = compare_costs(dc, oc, COST_RTOL_FP32)
+    print(f"tcgen05 H={H} injected: {ok.mean():.5f} within rtol, max rel {rel.max():.3g}, flips {flips}")
+    assert ok.mean() >= 0.999 and flips <= 2
+    assert np.array_equal(dstored, ostored)
+
+
 # ------------------------------------------------------- full-size checks
 def test_c1_full_size_costs_against_oracle():
     """BASELINE c1 size (K=16384, T=100): every per-sample cost vs the oracle (fp64 and fp32)."""
