@@ -25,7 +25,7 @@ PLAN_ATOL_FP32 = 1e-5
 # tolerance against the float restatement, and against the double reference
 # it must be no worse than fp32 arithmetic itself (the float restatement
 # differs from the double one by ~9e-5 per update at c0; tools/accuracy.py,
-# profiles/r02/accuracy.jsonl).
+# profiles/r02c/accuracy.jsonl).
 PLAN_ATOL_FP32_VS_FLOAT_ORACLE = 1e-5
 
 
@@ -425,13 +425,16 @@ def test_full_iteration_parity_c2():
     iterate_against_oracles(g, o32, o64, w.x0[0].copy(), 2, threads=16, label="c2")
 
 
-def test_fleet_member_parity_c3():
+@pytest.mark.parametrize("C", [4, 16])
+def test_fleet_member_parity_c3(C):
     """A c3-shaped fleet (K = 2048, T = 100, perturbed maps): controller 2 of a
-    4-controller fleet against the restatement run with the same seed and its
-    perturbed map read back from the device."""
-    w = workload.make("c3", controllers=4)
+    C-controller fleet against the restatement run with the same seed and its
+    perturbed map read back from the device.  C = 16 (32 768 samples in all)
+    runs the fleet on the tcgen05 K1, as the 512-controller c3 does."""
+    w = workload.make("c3", controllers=C)
     f = Controller(w.params, w.bounds, w.sg, w.cost, hidden=32, precision="fp32", noise="ref_splitmix",
-                   n_controllers=4)
+                   n_controllers=C)
+    assert ("rollout_umma_kernel" in f.kernel_variant) == (C == 16), f.kernel_variant
     f.set_mlp(w.mlp)
     f.set_costmap(w.costmap)
     f.perturb_fleet_costmaps(0.02, workload.SEED)
