@@ -251,6 +251,9 @@ struct Handle final : HandleBase {
     if (use_umma)
       std::snprintf(buf, sizeof(buf), "rollout_umma_kernel<f32,H=%d,noise=%d> (tcgen05.mma f16x3 M=128, TMEM accumulators, chunk 128, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);
+    else if (use_tc && tc_pair_used == 2)
+      std::snprintf(buf, sizeof(buf), "rollout_tc_split_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, 8 samples per warp on the n dimension, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
+                    H, cfg.noise_mode, n_chunks, n_groups);
     else if (use_tc && tc_pair_used == 1)
       std::snprintf(buf, sizeof(buf), "rollout_tc_pair_kernel<f32,H=%d,noise=%d> (mma.sync f16x3, chunk 16 per warp pair, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);

@@ -4,6 +4,7 @@
 // in parallel.
 #include "rollout_tc.cuh"
 #include "rollout_tc_pair.cuh"
+#include "rollout_tc_split.cuh"
 #include "ws_launch.hpp"
 
 #include <algorithm>
@@ -104,6 +105,38 @@ cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
   g_tc_last_pair = 1;
   return launch_k1(kern, grid, 64 * kTcPairs, smem, stream, a, frag);
 }
+// The sample-split warp pair (rollout_tc_split.cuh): H = 32, eps' on chip,
+// no trace, only when the whole grid is resident at once.  MPPI_TC_SPLIT=1
+// selects it whenever it fits.
+constexpr int kTcSplitPairs = 1;  // warp pairs (chunks) per CTA
+template <int Mode, bool STAB>
+bool split_fits(int T, int n_chunks, int ctrls) {
+  const char* e = std::getenv("MPPI_TC_SPLIT");
+  if (!e || std::atoi(e) == 0) return false;
+  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB>;
+  const size_t smem = mppi_dev::tc_split_smem_bytes(T, kTcSplitPairs);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64 * kTcSplitPairs, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const long long ctas = static_cast<long long>((n_chunks + kTcSplitPairs - 1) / kTcSplitPairs) * ctrls;
+  return ctas <= static_cast<long long>(per_sm) * sms;
+}
+template <int Mode, bool STAB>
+cudaError_t go_split(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
+                     cudaStream_t stream) {
+  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB>;
+  const size_t smem = mppi_dev::tc_split_smem_bytes(a.T, kTcSplitPairs);
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const dim3 grid((n_chunks + kTcSplitPairs - 1) / kTcSplitPairs, ctrls);
+  g_tc_last_pair = 2;
+  return launch_k1(kern, grid, 64 * kTcSplitPairs, smem, stream, a, frag);
+}
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (tc_min_ctas CTAs of 4 warps per SM); larger launches regenerate it from
 // the counters.
@@ -127,6 +160,8 @@ cudaError_t go(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int 
                                                       ctas <= per_sm * static_cast<long long>(sms));
   g_tc_last_pair = 0;
   if constexpr (H == 32 && MT == 1) {
+    if (!a.trace_states && split_fits<Mode, STAB>(a.T, n_chunks, ctrls))
+      return go_split<Mode, STAB>(a, frag, n_chunks, ctrls, stream);
     if (!a.trace_states && pair_fits<Mode, STAB>(a.T, n_chunks, ctrls))
       return go_pair<Mode, STAB>(a, frag, n_chunks, ctrls, stream);
   }

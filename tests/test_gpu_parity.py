@@ -661,6 +661,22 @@ def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
     assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
 
 
+@pytest.mark.parametrize("K,T,noise,form", [(1920, 100, "philox", "baseline"), (4096, 100, "philox", "baseline"),
+                                            (1000, 37, "philox", "reference"), (500, 20, "ref_splitmix", "baseline")])
+def test_split_kernel_bit_identical_to_single_warp(K, T, noise, form):
+    """The sample-split K1 (one chunk per two warps, 8 samples each on the mma
+    n dimension, movmatrix transposes between layers; rollout_tc_split.cuh)
+    performs exactly the single-warp tensor-core kernel's operations: costs,
+    plans and controls are bit-identical (odd T, a ragged last chunk, the
+    side-slip term and the reference noise stream included)."""
+    res = {f: _run_script(_PAIR_SCRIPT, [K, T, noise, form], {"MPPI_TC_SPLIT": f, "MPPI_TC_PAIR": "0"})
+           for f in ("0", "1")}
+    assert "rollout_tc_split_kernel" in res["1"]["variant"], res["1"]["variant"]
+    assert "rollout_tc_kernel" in res["0"]["variant"], res["0"]["variant"]
+    assert res["0"]["costs"] == res["1"]["costs"]
+    assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
+
+
 def test_tail_grid_does_not_change_results():
     """Each merged element is summed by one CTA in a fixed row order, so the
     tail's grid size cannot change a bit of the plan."""
