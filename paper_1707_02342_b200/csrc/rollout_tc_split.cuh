@@ -39,6 +39,13 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   return y;
 }
 
+// p ? a : b as one selp (never a branch)
+__device__ __forceinline__ float fsel_if(int p, float a, float b) {
+  float r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\tselp.f32 %0, %1, %2, q;\n\t}" : "=f"(r) : "f"(a), "f"(b), "r"(p));
+  return r;
+}
+
 // accumulator tile (rows g, g+8 = hidden units; columns 2t, 2t+1 = samples)
 // -> activation -> fp16 hi/lo words transposed to (hidden 2t, 2t+1; sample g):
 // h0/l0 from rows g (the k-slice's first 8 units), h1/l1 from rows g+8
@@ -141,6 +148,11 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
   const uint64_t seed = a.seeds[ctrl], iteration = a.iters[ctrl];
   float zc0 = 0.f, zc1 = 0.f;
   float v0c, v1c, coup_t;
+  const uint32_t s_eps_base = static_cast<uint32_t>(__cvta_generic_to_shared(s_eps + row));
+  // v_t = g(u_t + eps_t) and the coupling of step t (controller.cpp:86-101).
+  // (At one warp per scheduler the noise draws here cost less than a
+  // prologue computing the batch up front, tc_eps_prologue: c0 72.2 vs
+  // 73.3 us; profiles/r02d.)
   auto produce_v = [&](int t, bool even) {
     float e0, e1;
     if constexpr (Mode == kPhilox) {
@@ -161,7 +173,14 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
     const float u0 = s_plan[2 * t], u1 = s_plan[2 * t + 1];
     e0 = zm ? e0 - u0 : e0;
     e1 = zm ? e1 - u1 : e1;
-    if (t < T && own) s_eps[t * 16 + row] = make_float2(e0, e1);
+    // owner-only store as a predicated st.shared (a C++ `if` on the lane
+    // index compiles to a divergent branch + reconvergence in every step)
+    {
+      const uint32_t addr = s_eps_base + 8u * static_cast<uint32_t>(t * 16);
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.shared.v2.f32 [%0], {%1, %2};\n\t}" ::"r"(addr),
+                   "f"(e0), "f"(e1), "r"(static_cast<int>(t < T && own))
+                   : "memory");
+    }
     const float v0 = u0 + e0, v1 = u1 + e1;
     const float uv = __fmul_rn(__fmul_rn(u0, v0), inv_s0) + __fmul_rn(__fmul_rn(u1, v1), inv_s1);
     const float uu = __fmul_rn(__fmul_rn(u0, u0), inv_s0) + __fmul_rn(__fmul_rn(u1, u1), inv_s1);
@@ -186,6 +205,7 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
   MapTaps<float> q{};
   float p_roll = 0.f, p_vx = 0.f, p_vy = 0.f, p_coup = 0.f;
   const int quad0 = lane & ~3;
+  const int sel_0 = t4 == 0, sel_2 = t4 == 2, sel_lo = t4 < 2;
   produce_v(0, true);
 
   auto step = [&](int t, auto even_tag) {
@@ -200,8 +220,9 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
     // ---- layer 1: B operand = input pair t4 of sample g: (roll, vx), (vy, thd), (v0, v1), (1, 0)
     uint32_t xh, xl;
     {
-      const float bx = t4 == 0 ? roll : t4 == 1 ? vy : t4 == 2 ? v0c : 1.f;
-      const float by = t4 == 0 ? vx : t4 == 1 ? thd : t4 == 2 ? v1c : 0.f;
+      // (selp: the ternaries on the lane index compiled to divergent branches)
+      const float bx = fsel_if(sel_lo, fsel_if(sel_0, roll, vy), fsel_if(sel_2, v0c, 1.f));
+      const float by = fsel_if(sel_lo, fsel_if(sel_0, vx, thd), fsel_if(sel_2, v1c, 0.f));
       split2(bx, by, xh, xl);
     }
     uint32_t x2h[2][2], x2l[2][2];  // layer-2 B operand [k-tile][b0, b1]

@@ -106,24 +106,31 @@ cudaError_t go_pair(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag,
   return launch_k1(kern, grid, 64 * kTcPairs, smem, stream, a, frag);
 }
 // The sample-split warp pair (rollout_tc_split.cuh): H = 32, eps' on chip,
-// no trace, only when the whole grid is resident at once.  MPPI_TC_SPLIT=1
-// selects it whenever it fits.
+// no trace.  Default while its warps fit one per scheduler (2 chunks' worth
+// of warps per 4 schedulers of an SM): there a warp's step is its own chain
+// and the split halves the MLP part of it (c0 K1 86.8 -> 72.2 us, K = 4096
+// 86.6 -> 73.2); with two warps on a scheduler the single-warp kernel's
+// lower instruction count per sample wins (K = 6144 +5 %, K = 8192 +5 %,
+// profiles/r02d).  MPPI_TC_SPLIT=0 disables it, =1 uses it whenever the
+// grid is resident at once.
 constexpr int kTcSplitPairs = 1;  // warp pairs (chunks) per CTA
 template <int Mode, bool STAB>
 bool split_fits(int T, int n_chunks, int ctrls) {
   const char* e = std::getenv("MPPI_TC_SPLIT");
-  if (!e || std::atoi(e) == 0) return false;
+  const int mode = e ? std::atoi(e) : -1;
+  if (mode == 0) return false;
   auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB>;
   const size_t smem = mppi_dev::tc_split_smem_bytes(T, kTcSplitPairs);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long ctas = static_cast<long long>((n_chunks + kTcSplitPairs - 1) / kTcSplitPairs) * ctrls;
+  if (mode != 1 && 2LL * kTcSplitPairs * ctas > 4LL * sms) return false;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 64 * kTcSplitPairs, smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  const long long ctas = static_cast<long long>((n_chunks + kTcSplitPairs - 1) / kTcSplitPairs) * ctrls;
   return ctas <= static_cast<long long>(per_sm) * sms;
 }
 template <int Mode, bool STAB>

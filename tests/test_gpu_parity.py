@@ -574,8 +574,9 @@ def test_kernel_variant_and_launch_count():
     n0 = g.launch_count
     g.mpc_step(w.x0[0])
     # the fp32 H = 32 vehicle step: the x0 fetch, the tensor-core K1 (its
-    # programmatic dependent), the group merge and the tail
-    assert "rollout_tc_kernel<f32,H=32,MT=1" in g.kernel_variant  # one warp per 16-sample chunk
+    # programmatic dependent), the group merge and the tail; at c0 the K1 is
+    # the sample-split warp pair (its warps fit one per scheduler)
+    assert "rollout_tc_split_kernel<f32,H=32" in g.kernel_variant, g.kernel_variant
     assert g.launch_count - n0 == 4
     w64 = workload.make("c2", samples=256, horizon_steps=20)
     g64, _ = pair(w64, "fp32", "philox")
@@ -621,8 +622,9 @@ def test_onchip_and_regenerated_eps_bit_identical(K):
     from the counters otherwise — a choice that depends on the rank's share of
     the samples.  Both numerator passes (and the warp-pair kernel's) sum the
     chunk rows in one order, so costs, plans and controls are bit-identical
-    (MPPI_TC_STORE=0 / 1 force the two; the pair kernel is off here)."""
-    res = {f: _run_script(_TAIL_SCRIPT, [K], {"MPPI_TC_STORE": f, "MPPI_TC_PAIR": "0"}) for f in ("0", "1")}
+    (MPPI_TC_STORE=0 / 1 force the two; the pair and split kernels are off
+    here)."""
+    res = {f: _run_script(_TAIL_SCRIPT, [K], {"MPPI_TC_STORE": f, "MPPI_TC_PAIR": "0", "MPPI_TC_SPLIT": "0"}) for f in ("0", "1")}
     assert res["0"]["costs"] == res["1"]["costs"]
     assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
     assert all(r["it"] == 3 and r["launches"] == 13 for r in res.values())  # 1 + 3 x (x0 fetch, K1, group merge, tail)
@@ -654,7 +656,8 @@ def test_pair_kernel_bit_identical_to_single_warp(K, T, noise, form):
     tensor-core kernel's operations: costs, plans and controls are
     bit-identical (odd T, a ragged last chunk, the side-slip cost term and the
     reference noise stream included)."""
-    res = {f: _run_script(_PAIR_SCRIPT, [K, T, noise, form], {"MPPI_TC_PAIR": f}) for f in ("0", "1")}
+    res = {f: _run_script(_PAIR_SCRIPT, [K, T, noise, form], {"MPPI_TC_PAIR": f, "MPPI_TC_SPLIT": "0"})
+           for f in ("0", "1")}
     assert "rollout_tc_pair_kernel" in res["1"]["variant"], res["1"]["variant"]
     assert "rollout_tc_kernel" in res["0"]["variant"], res["0"]["variant"]
     assert res["0"]["costs"] == res["1"]["costs"]
