@@ -262,50 +262,6 @@ __device__ __forceinline__ void tc_sum_cross(const float (&c)[NK][4], float (&ou
   out[3] = y.y;
 }
 
-// The chunk's whole eps' batch (eps - U for the zero-mean samples, the batch
-// rollout_batch leaves; controller.cpp:86-101) into s_eps [T][16], computed
-// by all of the CTA's threads before the rollout: the noise does not depend
-// on the state, so its Philox / Box-Muller chains leave the step loop (where
-// they lengthened a lone warp's step) and run here with full ILP.  Same
-// expressions as the per-step draw, so the values are bit-identical to it.
-template <int Mode>
-__device__ __forceinline__ void tc_eps_prologue(const RolloutArgs<float>& a, int ctrl, int chunk,
-                                                const float* s_plan, float2* s_eps, int tid, int nthr) {
-  const int T = a.T;
-  auto put = [&](int r, int t, bool zm, float e0, float e1) {
-    const float u0 = s_plan[2 * t], u1 = s_plan[2 * t + 1];
-    e0 = zm ? e0 - u0 : e0;
-    e1 = zm ? e1 - u1 : e1;
-    s_eps[t * 16 + r] = make_float2(e0, e1);
-  };
-  if constexpr (Mode == kPhilox) {
-    const uint64_t seed = a.seeds[ctrl], iteration = a.iters[ctrl];
-    const int P = (T + 1) >> 1;
-    for (int idx = tid; idx < 16 * P; idx += nthr) {
-      const int r = idx & 15, p = idx >> 4;
-      const int k = chunk * 16 + r;
-      const int kn = (k < a.K) ? k : 0;
-      const bool zm = k >= a.zero_start;
-      const uint4 d = philox_draw(seed, iteration, static_cast<uint32_t>(kn), static_cast<uint32_t>(p));
-      float z0, z1, z2, z3;
-      philox_box_muller(d.x, d.y, z0, z1);
-      philox_box_muller(d.z, d.w, z2, z3);
-      put(r, 2 * p, zm, a.scale0 * z0, a.scale1 * z1);
-      if (2 * p + 1 < T) put(r, 2 * p + 1, zm, a.scale0 * z2, a.scale1 * z3);
-    }
-  } else {
-    for (int idx = tid; idx < 16 * T; idx += nthr) {
-      const int r = idx & 15, t = idx >> 4;
-      const int k = chunk * 16 + r;
-      const int kn = (k < a.K) ? k : 0;
-      NoiseStream<float, Mode> ns = make_noise<float, Mode>(a, ctrl, kn);
-      float e0, e1;
-      ns.eps(t, e0, e1);
-      put(r, t, k >= a.zero_start, e0, e1);
-    }
-  }
-}
-
 template <int MT>
 struct TcStage {
   uint32_t in[MT][2][64];  // [tile][hi/lo][tc_in_word]

@@ -151,8 +151,8 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
   const uint32_t s_eps_base = static_cast<uint32_t>(__cvta_generic_to_shared(s_eps + row));
   // v_t = g(u_t + eps_t) and the coupling of step t (controller.cpp:86-101).
   // (At one warp per scheduler the noise draws here cost less than a
-  // prologue computing the batch up front, tc_eps_prologue: c0 72.2 vs
-  // 73.3 us; profiles/r02d.)
+  // prologue computing the whole batch up front: c0 72.2 vs 73.3 us;
+  // profiles/r02d.)
   auto produce_v = [&](int t, bool even) {
     float e0, e1;
     if constexpr (Mode == kPhilox) {
