@@ -45,7 +45,9 @@ __host__ __device__ constexpr int umma_sw_rcp() {
 // the 66 KB per-tile footprint, so CTA pairs hold four tiles per SM where
 // single-tile CTAs fit three.  Measured (-DMPPI_UMMA_TPC=2, H = 64, 128
 // registers): c2 K1 1165 -> 1118 us (one wave instead of 1.15), but
-// K = 32768 +17 % and K = 131072 +13 % — kept as a build option.
+// K = 32768 +17 % and K = 131072 +13 %.  So the launcher picks the two-tile
+// CTAs at H = 64 only when they fit the grid in one wave and single tiles
+// do not (umma_launch.cuh: the c2 band, 445 .. 592 tiles per controller set).
 template <int H>
 __host__ __device__ constexpr int umma_tiles_per_cta() {
 #ifdef MPPI_UMMA_TPC
@@ -57,17 +59,17 @@ __host__ __device__ constexpr int umma_tiles_per_cta() {
 // resident CTAs per SM the register budget is sized for: four tiles at H = 32
 // (128 registers), three at H = 64 (its shared-memory footprint allows no
 // more), two two-tile CTAs
-template <int H>
+template <int H, int TPC = umma_tiles_per_cta<H>()>
 __host__ __device__ constexpr int umma_min_ctas() {
 #ifdef MPPI_UMMA_CTAS
   return MPPI_UMMA_CTAS;
 #else
-  return umma_tiles_per_cta<H>() == 2 ? 2 : (H == 32 ? 4 : 3);
+  return TPC == 2 ? 2 : (H == 32 ? 4 : 3);
 #endif
 }
 // accumulators per tile: [0, H) hi*hi, [H, 2H) cross terms
-template <int H>
-__host__ __device__ constexpr int umma_tmem_cols() { return 2 * H * umma_tiles_per_cta<H>(); }
+template <int H, int TPC = umma_tiles_per_cta<H>()>
+__host__ __device__ constexpr int umma_tmem_cols() { return 2 * H * TPC; }
 
 // Byte offset of element (row, k) of a K = 16 fp16 tile in the canonical
 // K-major, no-swizzle layout: 8-row x 16-byte core matrices, the two K halves
@@ -214,20 +216,19 @@ __host__ __device__ constexpr size_t umma_tile_region_bytes() {
   const size_t stage = sizeof(double) * kTcTB * 2 * kUmmaThreads;
   return tiles > stage ? tiles : stage;
 }
-template <int H>
+template <int H, int TPC = umma_tiles_per_cta<H>()>
 __host__ __device__ constexpr size_t umma_smem_bytes(int T) {
   const size_t plan = (sizeof(float) * (2 * T + 2) + 127) & ~size_t(127);
-  return plan + UmmaLayout<H>::BYTES + umma_tiles_per_cta<H>() * umma_tile_region_bytes<H>() + 128;
+  return plan + UmmaLayout<H>::BYTES + TPC * umma_tile_region_bytes<H>() + 128;
 }
 // a named barrier over the 128 threads of tile `tile` (ids 1 ..; 0 is __syncthreads)
 __device__ __forceinline__ void umma_tile_bar(int tile) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + tile), "n"(kUmmaThreads) : "memory");
 }
 
-template <int H, int Mode, bool STAB, bool TRACE>
-__global__ void __launch_bounds__(kUmmaThreads * umma_tiles_per_cta<H>(), umma_min_ctas<H>()) rollout_umma_kernel(
+template <int H, int Mode, bool STAB, bool TRACE, int TPC = umma_tiles_per_cta<H>()>
+__global__ void __launch_bounds__(kUmmaThreads * TPC, umma_min_ctas<H, TPC>()) rollout_umma_kernel(
     const __grid_constant__ RolloutArgs<float> a, const unsigned char* __restrict__ wimg) {
-  constexpr int TPC = umma_tiles_per_cta<H>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t s_taddr;
   __shared__ __align__(8) unsigned long long s_mbar_all[TPC];
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kUmmaThreads * umma_tiles_per_cta<H>(), umma_m
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      static_cast<uint32_t>(__cvta_generic_to_shared(&s_taddr))),
-                 "n"(umma_tmem_cols<H>()));
+                 "n"(umma_tmem_cols<H, TPC>()));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(kUmmaThreads * umma_tiles_per_cta<H>(), umma_m
   tc05_before_sync();
   __syncthreads();
   if (threadIdx.x < 32)  // (the allocating warp frees every tile's columns)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "n"(umma_tmem_cols<H>()));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_taddr), "n"(umma_tmem_cols<H, TPC>()));
   if (valid && !isfinite(cost)) s_bad = 1;
   // rho = min, eta = sum exp(-(S - rho) / lambda) over the chunk (warps in order)
   Acc m = warp_min(valid ? cost : Acc(INFINITY));

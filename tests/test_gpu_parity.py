@@ -680,6 +680,36 @@ def test_split_kernel_bit_identical_to_single_warp(K, T, noise, form):
     assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
 
 
+_C2_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+from paper_1707_02342_b200 import workload
+from paper_1707_02342_b200.api import Controller
+K, T = int(sys.argv[2]), int(sys.argv[3])
+w = workload.make('c2', samples=K, horizon_steps=T)
+g = Controller(w.params, w.bounds, w.sg, w.cost, hidden=64, precision='fp32', noise='philox')
+g.set_mlp(w.mlp); g.set_costmap(w.costmap)
+g.plan = np.random.default_rng(5).uniform(-0.4, 0.4, (T, 2))
+costs = g.rollout_batch(w.x0[0])
+u = [g.mpc_step(w.x0[0]).tolist() for _ in range(2)]
+print(json.dumps({'costs': costs.tolist(), 'plan': g.plan.tolist(), 'u': u, 'variant': g.kernel_variant}))
+"""
+
+
+@pytest.mark.parametrize("K,T", [(65536, 150), (60000, 31)])
+def test_umma_two_tile_ctas_bit_identical(K, T):
+    """The tcgen05 K1 at H = 64 runs two 128-sample tiles per CTA (one shared
+    weight copy) when that fits the grid in one wave and single tiles do not
+    (the c2 band).  Each tile performs the single-tile CTA's operations, so
+    costs, plans and controls are bit-identical either way (c2 itself and a
+    ragged K with an odd tile count)."""
+    res = {f: _run_script(_C2_SCRIPT, [K, T], {"MPPI_UMMA_TPC2": f}) for f in ("0", "1")}
+    assert "rollout_umma_kernel<f32,H=64" in res["0"]["variant"], res["0"]["variant"]
+    assert res["0"]["costs"] == res["1"]["costs"]
+    assert res["0"]["plan"] == res["1"]["plan"] and res["0"]["u"] == res["1"]["u"]
+
+
 def test_tail_grid_does_not_change_results():
     """Each merged element is summed by one CTA in a fixed row order, so the
     tail's grid size cannot change a bit of the plan."""
