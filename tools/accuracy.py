@@ -74,7 +74,7 @@ def one(cfg, iters):
     print(json.dumps({"cfg": cfg, "kernel": g.kernel_variant, "max": agg, "per_iteration": rows}), flush=True)
 
 
-VARIANTS = [{}, {"MPPI_TC_W3_SHIFT": "0"}, {"MPPI_TC_PAIR": "1"}, {"MPPI_KERNEL": "ws"}]
+VARIANTS = [{}, {"MPPI_TC_W3_SHIFT": "0"}, {"MPPI_TC_PAIR": "1", "MPPI_TC_SPLIT": "0"}, {"MPPI_KERNEL": "ws"}]
 
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "one":
@@ -84,7 +84,7 @@ if __name__ == "__main__":
     for env in VARIANTS:
         for cfg in cfgs:
             e = dict(os.environ)
-            for k in ("MPPI_KERNEL", "MPPI_TC_PAIR", "MPPI_TC_W3_SHIFT"):
+            for k in ("MPPI_KERNEL", "MPPI_TC_PAIR", "MPPI_TC_SPLIT", "MPPI_TC_W3_SHIFT"):
                 e.pop(k, None)
             e.update(env)
             r = subprocess.run([sys.executable, __file__, "one", cfg, "6" if cfg == "c0" else "3"], env=e,

@@ -5,7 +5,7 @@
 # of the tcgen05 K1 at c2 (H = 64) and K = 262144 (H = 32) with the mma.sync
 # K1 beside them, the config sweep and the accuracy study.
 # Usage: bash tools/gpu_evidence.sh TAG
-TAG=${1:-r02}
+TAG=${1:-r02d}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/nvsmi.txt 2>&1
