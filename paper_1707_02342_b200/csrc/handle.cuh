@@ -247,7 +247,7 @@ struct Handle final : HandleBase {
     }
   }
   std::string variant_name() const override {
-    char buf[160];
+    char buf[256];
     if (use_umma)
       std::snprintf(buf, sizeof(buf), "rollout_umma_kernel<f32,H=%d,noise=%d> (tcgen05.mma f16x3 M=128, TMEM accumulators, chunk 128, %d chunks, %d groups, group merge + tail kernels)",
                     H, cfg.noise_mode, n_chunks, n_groups);
@@ -1100,7 +1100,10 @@ struct Handle final : HandleBase {
         k1_pdl = which < 2 && use_tc && std::is_same<R, float>::value && cfg.weight_rule != MPPI_WEIGHT_CEM;
         if (k1_pdl) {
           if constexpr (std::is_same<R, float>::value) {
-            fetch_x0_kernel<><<<1, 32, 0, stream>>>(h_x0.p, d_x0.p, C * 8);
+            const int n4 = C * 2;  // (rows of 8 floats: two float4 each; pinned buffers are page-aligned)
+            const int threads = std::min(kFetchX0Block, (n4 + 31) / 32 * 32);
+            fetch_x0_kernel<><<<(n4 + threads - 1) / threads, threads, 0, stream>>>(
+                reinterpret_cast<const float4*>(h_x0.p), reinterpret_cast<float4*>(d_x0.p), n4);
             ++launches;
             CUDA_TRY(cudaGetLastError());
           }

@@ -59,13 +59,18 @@ struct RolloutArgs {
 };
 
 // The step graph's first node on the tensor-core path: the controllers'
-// states from the mapped pinned host buffer into device memory (one CTA, a
-// single PCIe round trip), with K1 launched as its programmatic dependent.
+// states from the mapped pinned host buffer into device memory, one float4
+// (half a controller's 8-float row) per thread, every PCIe read in flight at
+// once, with K1 launched as its programmatic dependent.  (A one-warp loop
+// over C x 8 floats serialised C / 4 PCIe round trips per thread: ~0.2 ms
+// for the 512-controller c3 fleet.)
 template <int kUnused = 0>
-__global__ void fetch_x0_kernel(const float* __restrict__ host_x0, float* __restrict__ x0, int n) {
+__global__ void fetch_x0_kernel(const float4* __restrict__ host_x0, float4* __restrict__ x0, int n4) {
   cudaTriggerProgrammaticLaunchCompletion();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x0[i] = host_x0[i];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n4) x0[i] = host_x0[i];
 }
+constexpr int kFetchX0Block = 256;
 
 template <class R, int Mode>
 __device__ __forceinline__ NoiseStream<R, Mode> make_noise(const RolloutArgs<R>& a, int ctrl, int k) {
