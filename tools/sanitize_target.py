@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """Small runs of every device kernel family for the device-checks build
 (tools/gpu_device_checks.sh; compute-sanitizer is closed on the GPU pool):
-the warp-pair K1 (c0 shape), the
-single-warp K1 with eps' on chip and regenerated (MT=1 / MT=2), the tcgen05 K1, the H=64 K1,
+the sample-split and warp-pair K1s (c0 shape), the
+single-warp K1 with eps' on chip and regenerated (MT=1 / MT=2), the tcgen05 K1 (one- and two-tile CTAs), the H=64 K1,
 the FFMA2 and generic K1, fp64, the group merge, the tail (closed loop with
 the device plant), a local 2-rank shard, the CEM rule, the bicycle model and
 the parity kernels.  Short horizons keep the sanitizer run in minutes."""
@@ -32,10 +32,14 @@ def run(cfg, K, T, steps=2, **kw):
     return c, w
 
 
+run("c0", 1920, 20)                                   # sample-split K1 (the c0 default)
+run("c0", 1000, 21)                                   # sample-split K1, ragged last chunk, odd T
+os.environ["MPPI_TC_SPLIT"] = "0"
 os.environ["MPPI_TC_PAIR"] = "1"
 run("c0", 1920, 20)                                   # warp-pair K1 (opt-in), one wave
 del os.environ["MPPI_TC_PAIR"]
 run("c0", 1920, 20)                                   # single-warp K1, predicated stage stores
+del os.environ["MPPI_TC_SPLIT"]
 run("c1", 4096, 20)                                   # MT=1, eps' on chip
 os.environ["MPPI_TC_STORE"] = "0"
 run("c1", 4096, 21)                                   # MT=1, regenerated eps', odd T
@@ -47,6 +51,9 @@ run("c4", 40000, 10, steps=1)                         # tcgen05 / TMEM K1
 run("c2", 2048, 12)                                   # H=64
 os.environ["MPPI_KERNEL"] = "umma"
 run("c2", 2001, 12)                                   # tcgen05 K1 at H=64, ragged last tile
+os.environ["MPPI_UMMA_TPC2"] = "1"
+run("c2", 1800, 12)                                   # two-tile CTAs, a half-empty last CTA (15 tiles)
+del os.environ["MPPI_UMMA_TPC2"]
 del os.environ["MPPI_KERNEL"]
 os.environ["MPPI_KERNEL"] = "ws"
 run("c1", 2048, 12)                                   # FFMA2 K1
