@@ -46,6 +46,20 @@ __device__ __forceinline__ float fsel_if(int p, float a, float b) {
   return r;
 }
 
+// L2 prefetch of the costmap rows under the position extrapolated one more
+// step, (2 p_{t+1} - p_t): the taps of x_{t+2} are read a step later, and with
+// the L2 cold (every newly visited line an HBM miss) that latency is about a
+// step.  Only cache state changes; the taps are still read by map_fetch.
+__device__ __forceinline__ void map_prefetch_l2(const MapDev<float>& m, float px, float py) {
+  float gx = mul_rn(sub_rn(px, m.x0), m.inv_res);
+  float gy = mul_rn(sub_rn(py, m.y0), m.inv_res);
+  gx = fminf(fmaxf(gx, 0.f), static_cast<float>(m.width - 2));
+  gy = fminf(fmaxf(gy, 0.f), static_cast<float>(m.height - 2));
+  const float* p = m.values + static_cast<size_t>(static_cast<int>(gy)) * m.width + static_cast<int>(gx);
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p + m.width));
+}
+
 // accumulator tile (rows g, g+8 = hidden units; columns 2t, 2t+1 = samples)
 // -> activation -> fp16 hi/lo words transposed to (hidden 2t, 2t+1; sample g):
 // h0/l0 from rows g (the k-slice's first 8 units), h1/l1 from rows g+8
@@ -73,7 +87,7 @@ struct TcSplitShared {
 };
 
 // The rollout of one warp half (HALF: chunk rows 8 HALF .. 8 HALF + 7).
-template <int NP, int Mode, bool STAB, int HALF>
+template <int NP, int Mode, bool STAB, bool PF, int HALF>
 __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const uint32_t* __restrict__ frag,
                                               float* s_plan, float2* s_eps, TcSplitShared& sh, int chunk,
                                               int bar_id) {
@@ -213,10 +227,12 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
     // pose of x_{t+1} and its costmap taps, a step ahead (as rollout_tc_kernel)
     float sn, cs;
     tc_sincos(th, sn, cs);
+    const float px_old = px, py_old = py;
     px = add_rn(px, mul_rn(sub_rn(mul_rn(cs, vx), mul_rn(sn, vy)), dt));
     py = add_rn(py, mul_rn(add_rn(mul_rn(sn, vx), mul_rn(cs, vy)), dt));
     th = add_rn(th, mul_rn(thd, dt));
     const MapTaps<float> q_next = map_fetch(map, px, py);
+    if constexpr (PF) map_prefetch_l2(map, 2.f * px - px_old, 2.f * py - py_old);
     // ---- layer 1: B operand = input pair t4 of sample g: (roll, vx), (vy, thd), (v0, v1), (1, 0)
     uint32_t xh, xl;
     {
@@ -365,7 +381,8 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
 #define MPPI_SPLIT_MINB 1
 #endif
 // grid = (ceil(chunks / NP), controllers), block = 64 * NP (NP warp pairs)
-template <int NP, int Mode, bool STAB>
+// PF: the two-steps-ahead L2 costmap prefetch (map_prefetch_l2)
+template <int NP, int Mode, bool STAB, bool PF>
 __global__ void __launch_bounds__(64 * NP, MPPI_SPLIT_MINB) rollout_tc_split_kernel(const __grid_constant__ RolloutArgs<float> a,
                                                                            const uint32_t* __restrict__ frag) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -384,9 +401,9 @@ __global__ void __launch_bounds__(64 * NP, MPPI_SPLIT_MINB) rollout_tc_split_ker
   cudaTriggerProgrammaticLaunchCompletion();  // one wave: the dependent may launch and wait
   float2* s_eps = s_eps_all + static_cast<size_t>(pair) * T * 16;
   if (half == 0)
-    tc_split_half<NP, Mode, STAB, 0>(a, frag, s_plan, s_eps, s_sh[pair], chunk, 1 + pair);
+    tc_split_half<NP, Mode, STAB, PF, 0>(a, frag, s_plan, s_eps, s_sh[pair], chunk, 1 + pair);
   else
-    tc_split_half<NP, Mode, STAB, 1>(a, frag, s_plan, s_eps, s_sh[pair], chunk, 1 + pair);
+    tc_split_half<NP, Mode, STAB, PF, 1>(a, frag, s_plan, s_eps, s_sh[pair], chunk, 1 + pair);
 }
 
 }  // namespace mppi_dev

@@ -119,7 +119,7 @@ bool split_fits(int T, int n_chunks, int ctrls) {
   const char* e = std::getenv("MPPI_TC_SPLIT");
   const int mode = e ? std::atoi(e) : -1;
   if (mode == 0) return false;
-  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB>;
+  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB, false>;
   const size_t smem = mppi_dev::tc_split_smem_bytes(T, kTcSplitPairs);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -133,16 +133,30 @@ bool split_fits(int T, int n_chunks, int ctrls) {
   }
   return ctas <= static_cast<long long>(per_sm) * sms;
 }
-template <int Mode, bool STAB>
-cudaError_t go_split(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
-                     cudaStream_t stream) {
-  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB>;
+// The split K1's two-steps-ahead L2 costmap prefetch pays while the samples
+// are sparse over the map (K1: c0 73.2 -> 67.1 us, K = 1024 -7.5 %, 2048
+// -8 %, 3072 -5.5 %) and costs where they are dense enough to keep the lines
+// warm (K = 4096 +4.2 %): on up to kSplitPfChunks chunks per controller
+// (profiles/r02d/pf_sweep.jsonl).  MPPI_SPLIT_PF=0 / 1 forces.
+constexpr int kSplitPfChunks = 192;
+template <int Mode, bool STAB, bool PF>
+cudaError_t go_split_pf(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
+                        cudaStream_t stream) {
+  auto kern = mppi_dev::rollout_tc_split_kernel<kTcSplitPairs, Mode, STAB, PF>;
   const size_t smem = mppi_dev::tc_split_smem_bytes(a.T, kTcSplitPairs);
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const dim3 grid((n_chunks + kTcSplitPairs - 1) / kTcSplitPairs, ctrls);
   g_tc_last_pair = 2;
   return launch_k1(kern, grid, 64 * kTcSplitPairs, smem, stream, a, frag);
+}
+template <int Mode, bool STAB>
+cudaError_t go_split(const mppi_dev::RolloutArgs<float>& a, const uint32_t* frag, int n_chunks, int ctrls,
+                     cudaStream_t stream) {
+  const char* e = std::getenv("MPPI_SPLIT_PF");
+  const bool pf = e ? std::atoi(e) != 0 : n_chunks <= kSplitPfChunks;
+  return pf ? go_split_pf<Mode, STAB, true>(a, frag, n_chunks, ctrls, stream)
+            : go_split_pf<Mode, STAB, false>(a, frag, n_chunks, ctrls, stream);
 }
 // eps' stays on chip when the grid still fits one wave with that footprint
 // (tc_min_ctas CTAs of 4 warps per SM); larger launches regenerate it from
