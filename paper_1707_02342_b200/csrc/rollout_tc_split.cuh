@@ -20,8 +20,11 @@
 //     A operand rows g+8 zero;
 //   * the four lanes of a quad run sample g's scalar path (noise, pose,
 //     costmap, cost) — lane t feeds input pair t of layer 1 directly from
-//     registers, and the outputs reach the quad by four shuffles: no
-//     shared-memory stage in the step loop.
+//     registers (selp), and the outputs reach the quad by four shuffles: no
+//     shared-memory stage, no barrier and no branch in the step loop;
+//   * optionally (PF, sparse sampling) an L2 prefetch of the costmap two
+//     steps ahead (map_prefetch_l2).
+// Used while its warps fit one per scheduler (tc_launch.cuh split_fits).
 // Every product, accumulation order and rounding is the single-warp kernel's
 // (a dot product's tensor-core sum does not depend on which operand holds
 // which factor; the reciprocal rule of tc_sw_rcp<32> — SFU for chunk rows
@@ -375,8 +378,9 @@ __device__ __forceinline__ void tc_split_half(const RolloutArgs<float>& a, const
   }
 }
 
-// Resident CTAs per SM the register budget is sized for: 1 (no cap, ~180
-// registers, no spills); a 7-CTA cap (c1's one wave) spills in the step loop
+// Resident CTAs per SM the register budget is sized for: 1 (no cap, ~200
+// registers, no spills; the kernel runs at <= 2 CTAs per SM); a 7-CTA cap
+// (c1's one wave) spills in the step loop
 #ifndef MPPI_SPLIT_MINB
 #define MPPI_SPLIT_MINB 1
 #endif
