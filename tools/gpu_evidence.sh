@@ -2,6 +2,7 @@
 # Round evidence for profiles/<TAG>/: bench lines (c1 with the CPU baseline,
 # the reference arm, c0/c2/c3), the ncu launch list of the c1 bench command,
 # one ncu --set full capture each of K1, the group merge and the tail at c1,
+# of the sample-split K1 at c0,
 # of the tcgen05 K1 at c2 (H = 64) and K = 262144 (H = 32) with the mma.sync
 # K1 beside them, the config sweep and the accuracy study.
 # Usage: bash tools/gpu_evidence.sh TAG
@@ -25,6 +26,7 @@ for k in rollout group_merge tail_kernel; do
   ncu -i $O/ncu_full_${k}_c1.ncu-rep --page details --csv > $O/ncu_full_${k}_c1_details.csv 2>&1
 done
 ncu -i $O/ncu_full_rollout_c1.ncu-rep --page source --csv --print-source sass > $O/ncu_full_rollout_c1_source.csv 2>&1
+bash tools/gpu_ncu_full.sh $TAG c0 0 rollout_tc_split > /dev/null 2>&1
 bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_umma > /dev/null 2>&1
 bash tools/gpu_ncu_full.sh $TAG c4 262144 rollout_umma > /dev/null 2>&1
 MPPI_KERNEL=mma bash tools/gpu_ncu_full.sh $TAG c2 0 rollout_tc > /dev/null 2>&1
