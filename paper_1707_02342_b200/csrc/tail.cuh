@@ -174,19 +174,34 @@ __device__ __forceinline__ void epilogue_fast(const EpilogueArgs<float>& a, cons
       s_h[j] = tanh_r(acc);
     }
     __syncwarp();
+    // (every operand of a unit's FMA chain is loaded before the chain starts:
+    // one shared-memory round trip instead of one per unrolled batch; the
+    // chain itself keeps the per-unit order)
+    float hv[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) hv[i] = s_h[i];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = lane + 32 * u;
+      float wv[H];
+#pragma unroll
+      for (int i = 0; i < H; ++i) wv[i] = w.w2t[i][j];
       float acc = w.b2[j];
-#pragma unroll 16
-      for (int i = 0; i < H; ++i) acc = fma_r(w.w2t[i][j], s_h[i], acc);
+#pragma unroll
+      for (int i = 0; i < H; ++i) acc = fma_r(wv[i], hv[i], acc);
       s_h[H + j] = tanh_r(acc);
     }
     __syncwarp();
     if (lane < 4) {
+      float wv[H], h2[H];
+#pragma unroll
+      for (int i = 0; i < H; ++i) {
+        wv[i] = w.w3t[i][lane];
+        h2[i] = s_h[H + i];
+      }
       float d = w.b3[lane];
-#pragma unroll 16
-      for (int i = 0; i < H; ++i) d = fma_r(w.w3t[i][lane], s_h[H + i], d);
+#pragma unroll
+      for (int i = 0; i < H; ++i) d = fma_r(wv[i], h2[i], d);
       s_d[lane] = d;
     }
     __syncwarp();
